@@ -1,0 +1,398 @@
+"""Pins of the CPU oracle (oracle/oracle.c) to things other than itself.
+
+Each test names the passage and the independent fact it uses: the SPEC worked
+example, textbook closed forms (PDG PMNS elements, two-flavour limits, the
+closed form of P_ee, Gauss-Legendre error constant, the sine-integral primitive
+of the bin integral), mpmath at 40 digits, numpy's leggauss, brute-force
+quadrature.  A plausible mistake anywhere in the oracle (dropped term, wrong
+sign or index, transposed matrix product, wrong pair order, wrong node
+mapping) fails at least one of them.  CPU only (no GPU marker).
+"""
+from __future__ import annotations
+
+import math
+import os
+from fractions import Fraction
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+EPS = np.finfo(np.float64).eps
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _mp_pmns(th12, th13, th23, dcp, anti=0):
+    """PDG closed-form PMNS elements (textbook, not a matrix product)."""
+    c12, s12 = mp.cos(th12), mp.sin(th12)
+    c13, s13 = mp.cos(th13), mp.sin(th13)
+    c23, s23 = mp.cos(th23), mp.sin(th23)
+    e = mp.exp(1j * mp.mpf(dcp))
+    V = mp.matrix([[c12 * c13, s12 * c13, s13 / e],
+                   [-s12 * c23 - c12 * s23 * s13 * e, c12 * c23 - s12 * s23 * s13 * e, s23 * c13],
+                   [s12 * s23 - c12 * c23 * s13 * e, -c12 * s23 - s12 * c23 * s13 * e, c23 * c13]])
+    if anti:
+        V = V.conjugate()
+    return V
+
+
+def _mp_phase(dm2, L, E):
+    # exact decimal value of the SPEC literal times the fp64 inputs
+    return mp.mpf("1.26693268") * mp.mpf(dm2) * mp.mpf(L) / (mp.mpf(E) / 1000)
+
+
+def _mp_prob_evolution(alpha, beta, p, L, E):
+    """|(V diag(exp(-i 2 Delta_i1)) V^dagger)_{beta alpha}|^2 — state evolution, not the P:633 sum."""
+    V = _mp_pmns(p["theta12"], p["theta13"], p["theta23"], p["delta_cp"], p.get("antineutrino", 0))
+    d21 = mp.mpf(p["dm2_21"])
+    d31 = mp.mpf(p["dm2_31"])
+    ph = [mp.mpf(0), _mp_phase(d21, L, E), _mp_phase(d31, L, E)]
+    amp = mp.mpc(0)
+    for i in range(3):
+        amp += mp.conj(V[alpha, i]) * V[beta, i] * mp.exp(-2j * ph[i])
+    return abs(amp) ** 2
+
+
+def _mp_pee_closed(p, L, E):
+    """Textbook closed form P_ee = 1 - c13^4 sin^2 2t12 sin^2 D21 - sin^2 2t13 (c12^2 sin^2 D31 + s12^2 sin^2 D32)."""
+    t12, t13 = mp.mpf(p["theta12"]), mp.mpf(p["theta13"])
+    d21, d31 = mp.mpf(p["dm2_21"]), mp.mpf(p["dm2_31"])
+    d32 = d31 - d21  # exact difference (S:237 definition); the oracle's fp64 difference is in the bound
+    D21, D31, D32 = (_mp_phase(d, L, E) for d in (d21, d31, d32))
+    return (1 - mp.cos(t13) ** 4 * mp.sin(2 * t12) ** 2 * mp.sin(D21) ** 2
+            - mp.sin(2 * t13) ** 2 * (mp.cos(t12) ** 2 * mp.sin(D31) ** 2
+                                      + mp.sin(t12) ** 2 * mp.sin(D32) ** 2))
+
+
+def _cond_bound(p, L, E):
+    """Rounding bound of the fp64 general formula: each phase carries <= 5 roundings
+    (product, quotient, dm2_32 difference), |dP/dDelta_ij| <= 4|X_ij|*2, plus 2e-15 for the sum."""
+    absX = 0.25  # |V_ai V_bi V_aj V_bj| <= 1/4 for unitary V (|V_ai|^2+|V_aj|^2 <= 1)
+    s = 0.0
+    for dm2 in (p["dm2_21"], p["dm2_31"], p["dm2_31"] - p["dm2_21"]):
+        s += 8 * absX * 5 * EPS * abs(1.26693268 * dm2 * L / (E / 1000.0))
+    return 2e-15 + s
+
+
+# ----------------------------------------------------------------------------- PMNS
+def test_pmns_zero_angles_is_identity():
+    # S:258 [TRIVIAL]
+    V = oracle.pmns(0, 0, 0, 0)
+    assert np.array_equal(V, np.eye(3, dtype=complex))
+
+
+def test_pmns_matches_pdg_closed_form_elements():
+    # PDG textbook element formulas pin the product order R23.U13.R12
+    # and the e^{-i delta} placement; a transposed or reordered product fails.
+    g = synth.rng(11)
+    mp.mp.dps = 30
+    for _ in range(50):
+        th = g.uniform(0, np.pi / 2, 3)
+        d = g.uniform(0, 2 * np.pi)
+        anti = int(g.random() < 0.5)
+        V = oracle.pmns(*th, d, anti)
+        Vr = _mp_pmns(*th, d, anti)
+        for a in range(3):
+            for i in range(3):
+                assert abs(V[a, i] - complex(Vr[a, i])) < 4e-16
+
+
+def test_pmns_unitary_and_theta13_zero():
+    g = synth.rng(12)
+    for _ in range(200):
+        th = g.uniform(0, np.pi / 2, 3)
+        V = oracle.pmns(*th, g.uniform(0, 2 * np.pi), int(g.random() < 0.5))
+        assert np.max(np.abs(V @ V.conj().T - np.eye(3))) < 1e-15
+        assert np.max(np.abs(V.conj().T @ V - np.eye(3))) < 1e-15
+    V = oracle.pmns(0.6, 0.0, 0.8, 1.0)
+    assert V[0, 2] == 0  # S:260-261 [DERIVED]
+
+
+def test_pmns_antineutrino_is_conjugate():
+    V = oracle.pmns(0.5, 0.15, 0.7, 1.3, 0)
+    Vb = oracle.pmns(0.5, 0.15, 0.7, 1.3, 1)
+    assert np.array_equal(Vb, V.conj())
+
+
+# ----------------------------------------------------------------------------- phase
+def test_phase_spec_worked_example():
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "spec_osc_phase_example.txt"))
+            if l.strip() and not l.startswith("#")]
+    for dm2, L, E, printed in rows:
+        got = oracle.phase(float(dm2), float(L), float(E))
+        assert abs(got - float(printed)) < 5e-9  # the printed value has 6 digits
+        exact = Fraction("1.26693268") * Fraction(dm2) * Fraction(L) / (Fraction(E) / 1000)
+        assert abs(Fraction(got) - exact) <= Fraction(EPS) * exact
+
+
+def test_phase_zero_and_linearity():
+    assert oracle.phase(2.5e-3, 0.0, 3.0) == 0.0  # S:267 [TRIVIAL]
+    g = synth.rng(13)
+    for _ in range(100):
+        dm2, L, E = g.uniform(1e-5, 3e-3), g.uniform(0.1, 300), g.uniform(1, 10)
+        # doubling L doubles Delta exactly (power-of-two scaling)
+        assert oracle.phase(dm2, 2 * L, E) == 2 * oracle.phase(dm2, L, E)
+
+
+# ----------------------------------------------------------------------------- P formula
+def test_prob_L0_is_kronecker_exactly():
+    g = synth.rng(14)
+    for _ in range(20):
+        p = synth.random_params(g)
+        for a in range(3):
+            for b in range(3):
+                assert oracle.prob(a, b, p, 0.0, g.uniform(1, 10)) == (1.0 if a == b else 0.0)
+
+
+def test_prob_zero_mixing_is_one():
+    p = dict(synth.CANONICAL, theta12=0.0, theta13=0.0, theta23=0.0)
+    for E in (1.0, 2.5, 7.0):
+        assert oracle.prob(0, 0, p, 52.5, E) == 1.0
+        assert oracle.prob(0, 1, p, 52.5, E) == 0.0
+
+
+def test_two_flavor_textbook_values():
+    # S:295-298
+    assert oracle.two_flavor(0.0, 2.5e-3, 52.5, 3.0) == 1.0
+    # choose E with Delta = pi/2
+    dm2, L = 2.5e-3, 1.0
+    E = 1.26693268 * dm2 * L * 1000.0 / (math.pi / 2)
+    th = 0.3
+    assert abs(oracle.two_flavor(th, dm2, L, E) - (1 - math.sin(2 * th) ** 2)) < 1e-15
+    assert abs(oracle.two_flavor(math.pi / 4, dm2, L, E)) < 1e-15
+
+
+def test_prob_two_flavor_limits():
+    # S:279 and SURVEY §8(c): theta13=0 -> two-flavour in (theta12, dm2_21);
+    # theta12=0 -> two-flavour in (theta13, dm2_31).  Pins the pair weights.
+    g = synth.rng(15)
+    for _ in range(200):
+        p = synth.random_params(g)
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        p0 = dict(p, theta13=0.0)
+        assert abs(oracle.prob(0, 0, p0, L, E)
+                   - oracle.two_flavor(p["theta12"], p["dm2_21"], L, E)) < 1e-14
+        p1 = dict(p, theta12=0.0)
+        assert abs(oracle.prob(0, 0, p1, L, E)
+                   - oracle.two_flavor(p["theta13"], p["dm2_31"], L, E)) < 1e-14
+
+
+def test_prob_unitarity_rows_and_columns():
+    # S:311 Σ_β P(α→β) = 1 and Σ_α P(α→β) = 1; pins the Im term sign and the
+    # conj placement of X_ij (a wrong sign breaks row sums off the e row).
+    g = synth.rng(16)
+    for _ in range(200):
+        p = synth.random_params(g)
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        P = np.array([[oracle.prob(a, b, p, L, E) for b in range(3)] for a in range(3)])
+        assert np.max(np.abs(P.sum(axis=1) - 1)) < 1e-13
+        assert np.max(np.abs(P.sum(axis=0) - 1)) < 1e-13
+        assert P.min() > -1e-13 and P.max() < 1 + 1e-12
+
+
+def test_prob_cpt():
+    # P_ab(delta) = P_ba(-delta); P(nubar, delta) = P(nu, -delta)
+    g = synth.rng(17)
+    for _ in range(100):
+        p = synth.random_params(g)
+        p["antineutrino"] = 0
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        pm = dict(p, delta_cp=-p["delta_cp"])
+        pb = dict(p, antineutrino=1)
+        for a in range(3):
+            for b in range(3):
+                assert abs(oracle.prob(a, b, p, L, E) - oracle.prob(b, a, pm, L, E)) < 1e-13
+                assert abs(oracle.prob(a, b, pb, L, E) - oracle.prob(a, b, pm, L, E)) < 1e-13
+
+
+def test_prob_amplitude_form_agrees():
+    # general formula vs amplitude form over 1000 draws (1e-12)
+    g = synth.rng(18)
+    for _ in range(1000):
+        p = synth.random_params(g)
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        a, b = int(g.integers(3)), int(g.integers(3))
+        assert abs(oracle.prob(a, b, p, L, E) - oracle.prob(a, b, p, L, E, amplitude=True)) < 1e-12
+
+
+def test_prob_vs_mpmath_state_evolution():
+    # 40-digit matrix evolution with PDG elements vs the fp64 general formula,
+    # within the rounding bound of the phase (R7).
+    mp.mp.dps = 40
+    g = synth.rng(19)
+    worst = 0.0
+    for _ in range(300):
+        p = synth.random_params(g)
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        a, b = int(g.integers(3)), int(g.integers(3))
+        ref = float(_mp_prob_evolution(a, b, p, L, E))
+        got = oracle.prob(a, b, p, L, E)
+        assert abs(got - ref) <= _cond_bound(p, L, E), (p, L, E, a, b)
+        worst = max(worst, abs(got - ref))
+    assert worst < 1e-12
+
+
+def test_pee_closed_form_and_canonical_point():
+    # S:280 canonical point; mpmath closed form and mpmath evolution agree to 30
+    # digits (pins the closed form itself), and the oracle agrees with both.
+    mp.mp.dps = 40
+    vals = [l.split() for l in open(os.path.join(GOLDEN, "spec_canonical_point.txt"))
+            if l.strip() and not l.startswith("#")][0]
+    th12, th13, th23, d, d21, d31, L, E = map(float, vals)
+    p = dict(theta12=th12, theta13=th13, theta23=th23, delta_cp=d, dm2_21=d21, dm2_31=d31)
+    closed = _mp_pee_closed(p, L, E)
+    evol = _mp_prob_evolution(0, 0, p, L, E)
+    assert abs(closed - evol) < mp.mpf("1e-30")
+    assert abs(float(closed) - 0.22339636878858184556) < 1e-18  # SURVEY Appendix value
+    assert abs(oracle.prob(0, 0, p, L, E) - float(closed)) < 1e-15
+    g = synth.rng(20)
+    for _ in range(300):
+        p = synth.random_params(g)
+        L, E = g.uniform(0, 300), g.uniform(1, 10)
+        got = oracle.prob(0, 0, p, L, E)
+        assert abs(got - float(_mp_pee_closed(p, L, E))) <= _cond_bound(p, L, E)
+
+
+def test_prob_array_matches_scalar_and_threads_bitwise():
+    g = synth.rng(21)
+    p = synth.random_params(g)
+    E = synth.random_energies(g, 5000)
+    P1 = oracle.prob_array(p, 52.5, E, nthreads=1)
+    P4 = oracle.prob_array(p, 52.5, E, nthreads=4)
+    assert np.array_equal(P1, P4)
+    assert all(P1[i] == oracle.prob(0, 0, p, 52.5, E[i]) for i in range(0, 5000, 97))
+
+
+# ----------------------------------------------------------------------------- Gauss-Legendre
+@pytest.mark.parametrize("n", list(range(1, 65)))
+def test_gauleg_vs_numpy_leggauss(n):
+    t, w = oracle.gauleg(n)
+    tn, wn = np.polynomial.legendre.leggauss(n)  # library routine (Golub-Welsch + Newton polish)
+    assert np.all(np.diff(t) > 0)  # ascending
+    assert np.max(np.abs(t - tn)) < 4e-16
+    # leggauss's own weights carry up to ~5e-15 error near the ends for n >= 40
+    # (checked against 40-digit Newton); the oracle's are within 2e-16 there.
+    assert np.max(np.abs(w - wn)) < 6e-15
+    assert np.array_equal(t, -t[::-1]) and np.array_equal(w, w[::-1])  # symmetric
+    assert abs(w.sum() - 2.0) < 1e-14
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 10, 16, 32])
+def test_gauleg_polynomial_exactness_and_error_constant(n):
+    # exact for x^k, k <= 2n-1; for x^{2n} the error equals the textbook GL
+    # remainder 2^{2n+1} (n!)^4 / ((2n+1) ((2n)!)^2)  (pins nodes AND weights)
+    t, w = oracle.gauleg(n)
+    for k in range(2 * n):
+        exact = 2.0 / (k + 1) if k % 2 == 0 else 0.0
+        assert abs(np.sum(w * t ** k) - exact) < 2e-14
+    mp.mp.dps = 30
+    rem = (mp.mpf(2) ** (2 * n + 1) * mp.factorial(n) ** 4
+           / ((2 * n + 1) * mp.factorial(2 * n) ** 2))
+    err = 2.0 / (2 * n + 1) - np.sum(w * t ** (2 * n))
+    assert abs(err - float(rem)) < 1e-13 + 1e-12 * float(rem)
+
+
+def test_gauleg_rejects_order0():
+    with pytest.raises(ValueError):
+        oracle.gauleg(0)
+
+
+# ----------------------------------------------------------------------------- bin integrals
+def _mp_bin_integral_exact(p, L, e0, e1):
+    """∫_{e0}^{e1} P_ee dE via the primitive ∫cos(a/E)dE = E cos(a/E) + a Si(a/E)."""
+    t12, t13 = mp.mpf(p["theta12"]), mp.mpf(p["theta13"])
+    W = {"21": mp.cos(t13) ** 4 * mp.sin(2 * t12) ** 2,
+         "31": mp.sin(2 * t13) ** 2 * mp.cos(t12) ** 2,
+         "32": mp.sin(2 * t13) ** 2 * mp.sin(t12) ** 2}
+    dm = {"21": mp.mpf(p["dm2_21"]), "31": mp.mpf(p["dm2_31"])}
+    dm["32"] = dm["31"] - dm["21"]
+
+    def F(E):
+        E = mp.mpf(E)
+        out = E
+        for ij in ("21", "31", "32"):
+            a = 2 * mp.mpf("1.26693268") * dm[ij] * mp.mpf(L) * 1000  # 2 Delta = a / E
+            # sin^2 D = (1 - cos(a/E)) / 2
+            out -= W[ij] * (E / 2 - (E * mp.cos(a / E) + a * mp.si(a / E)) / 2)
+        return out
+
+    return F(e1) - F(e0)
+
+
+def test_bins_zero_mixing_equal_width():
+    p = dict(synth.CANONICAL, theta12=0.0, theta13=0.0)
+    edges = synth.uniform_edges(37, 1.0, 10.0)
+    for n in (1, 4, 10):
+        b = oracle.gl_integrate(p, 52.5, edges, n)
+        assert np.max(np.abs(b / np.diff(edges) - 1)) < 2e-15
+
+
+def test_bins_cfg2_vs_sine_integral_closed_form():
+    # cfg2 geometry (1e5 bins x GL10): GL10 on 9e-5 MeV bins is exact to fp64,
+    # so the oracle's bins must equal the exact integral (SURVEY §8(c) pin).
+    mp.mp.dps = 30
+    c = synth.config("cfg2")
+    edges = c["edges"]
+    idx = np.r_[0:5, synth.rng(22).integers(0, edges.size - 1, 60), edges.size - 6:edges.size - 1]
+    bins = np.array([oracle.gl_integrate(c["params"], c["L_km"], edges[k:k + 2], 10)[0] for k in idx])
+    for k, got in zip(idx, bins):
+        ref = float(_mp_bin_integral_exact(c["params"], c["L_km"], edges[k], edges[k + 1]))
+        assert abs(got - ref) <= 2e-13 * abs(ref), (k, got, ref)
+
+
+def test_bins_gl_converges_to_closed_form_on_cfg1_bins():
+    # cfg1 bins are 0.09 MeV wide: GL5 is not the exact integral there (fast
+    # Delta_31 oscillation near 1 MeV), but GL32 is.
+    mp.mp.dps = 30
+    c = synth.config("cfg1")
+    e = c["edges"]
+    b32 = oracle.gl_integrate(c["params"], c["L_km"], e, 32)
+    b5 = oracle.gl_integrate(c["params"], c["L_km"], e, 5)
+    worst5 = 0.0
+    for k in range(0, 100, 3):
+        ref = float(_mp_bin_integral_exact(c["params"], c["L_km"], e[k], e[k + 1]))
+        assert abs(b32[k] - ref) <= 1e-13 * abs(ref)
+        worst5 = max(worst5, abs(b5[k] - ref) / ref)
+    assert 1e-3 < worst5 < 0.2  # GL5 is visibly inexact at 0.09 MeV bins (SURVEY finding 8)
+
+
+def test_bins_brute_force_quadrature_tiny():
+    mp.mp.dps = 25
+    g = synth.rng(23)
+    for _ in range(3):
+        p = synth.random_params(g, ordering_sign=True)
+        L = g.uniform(10, 80)
+        e0 = g.uniform(2.0, 8.0)
+        edges = np.sort(g.uniform(e0, e0 + 0.3, 4))  # narrow enough for GL32 to converge
+        b = oracle.gl_integrate(p, L, edges, 32)
+        for k in range(3):
+            f = lambda E: _mp_pee_closed(p, L, E)
+            ref = mp.quad(f, mp.linspace(edges[k], edges[k + 1], 40))
+            assert abs(b[k] - float(ref)) <= 1e-12 * abs(float(ref))
+
+
+# ----------------------------------------------------------------------------- batch
+def test_batch_is_weighted_sum_of_gl_integrals_and_chi2():
+    g = synth.rng(24)
+    pts = synth.points_uniform(g, 5, dict(theta12=(0.5, 0.65), theta13=(0.1, 0.2),
+                                          dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+    L = np.array([52.5, 215.0, 1.0])
+    om = np.array([1.0, 0.25, 3.0])
+    edges = synth.uniform_edges(23, 1.0, 10.0)
+    data = synth.pseudo_data(g, edges, om.sum())
+    S, X = oracle.batch(pts, L, om, edges, 6, data=data)
+    for p in range(5):
+        pp = dict(synth.CANONICAL, **{k: float(v[p]) for k, v in pts.items()})
+        T = sum(om[b] * oracle.gl_integrate(pp, L[b], edges, 6) for b in range(3))
+        assert np.max(np.abs(S[p] - T) / T) < 1e-15
+        assert abs(X[p] - np.sum((S[p] - data) ** 2 / data)) <= 1e-13 * X[p]
+    assert np.all(X >= 0)
+    # chi2 of a point against its own spectrum is exactly 0
+    S2, X2 = oracle.batch(pts, L, om, edges, 6, data=S[2])
+    assert X2[2] == 0.0
+    # thread count does not change a bit
+    S4, X4 = oracle.batch(pts, L, om, edges, 6, data=data, nthreads=3)
+    assert np.array_equal(S, S4) and np.array_equal(X, X4)
