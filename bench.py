@@ -1,0 +1,517 @@
+#!/usr/bin/env python
+"""Benchmark of the fused fp64 P_ee + Gauss-Legendre hot path on B200 (BASELINE.json metric:
+"energy points/sec (fp64 P_ee+GL) at 1/2/4/8 B200; % of HBM/FP64 roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5|cfg4|cfg2|cfg3]
+                    [--impl ours|reference]
+
+A step is one pass of the whole hot path over one batch:
+default workload cfg5 = 8 baselines x 1000 parameter points x 1e5 energies
+(1e4 bins x GL10), spectra + chi^2 per point, points sharded over ranks and the
+spectra/chi^2 gathered with NCCL (N > 1).  An "energy point" is one (parameter
+point x baseline x GL node) evaluation of P_ee.  Timing: CUDA events on the
+launching stream around each step, L2 flushed (256 MiB write) between steps,
+barrier + synchronize on both sides, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "energy points/sec (fp64 P_ee+GL)"
+UNIT = "energy points/s"
+
+# Algorithmic FP64-pipe work per energy point: three sin^2
+# terms x 13 FP64 instructions (rint 2, reduced argument 1, square 1, degree-8
+# minimax 8, weighted accumulate 1).  Per-node work (reciprocal, node position,
+# GL weight) is amortised over baselines and not counted.
+FP64_OPS_PER_EVAL = 39
+FP64_LANES_PER_SM = 64        # measured: tools/probe_fp64.cu, profiles/r01_probe_fp64.jsonl
+SM_COUNT = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg2", "cfg3"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--chunks", type=int, default=0, help="gather pipeline chunks (0 = auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- workloads
+def workload(name: str) -> dict:
+    c = synth.config(name)
+    if name in ("cfg4", "cfg5"):
+        P = c["points"]["theta12"].size
+        nb = c["edges"].size - 1
+        c["evals"] = P * c["L_km"].size * nb * c["order"]
+        c["bins_total"] = P * nb
+        c["desc"] = dict(workload="%s: %d baselines x %d parameter points x %d energies "
+                         "(%d bins x GL%d), spectra + chi2 per point" % (
+                             name, c["L_km"].size, P, nb * c["order"], nb, c["order"]),
+                         points=P, baselines=int(c["L_km"].size), bins=nb, order=c["order"])
+    elif name == "cfg2":
+        nb = c["edges"].size - 1
+        c["evals"] = nb * c["order"]
+        c["bins_total"] = nb
+        c["desc"] = dict(workload="cfg2: 1 parameter point, %d energies (%d bins x GL%d)" % (
+            nb * c["order"], nb, c["order"]), points=1, bins=nb, order=c["order"])
+    else:
+        c["evals"] = c["n"]
+        c["bins_total"] = 0
+        c["desc"] = dict(workload="cfg3: 1 parameter point, %d energies streamed from HBM "
+                         "(elementwise P_ee)" % c["n"], points=1, energies=c["n"])
+    return c
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The oracle (plain C, fp64) on this host's cores: the base contract's reference arm."""
+    if rank != 0:
+        return
+    import oracle
+    c = workload(args.workload)
+    nt = oracle.max_threads()
+    times, units = [], []
+
+    def one_step():
+        t0 = time.perf_counter()
+        if args.workload in ("cfg4", "cfg5"):
+            idx = np.arange(ns)
+            sub = synth.subset_points(c["points"], idx)
+            oracle.batch(sub, c["L_km"], c["omega"], c["edges"], c["order"], data=c["data"],
+                         nthreads=nt)
+            u = ns * c["L_km"].size * (c["edges"].size - 1) * c["order"]
+        elif args.workload == "cfg2":
+            e = c["edges"][:ns + 1]
+            oracle.gl_integrate(c["params"], c["L_km"], e, c["order"], nthreads=nt)
+            u = ns * c["order"]
+        else:
+            E = np.linspace(c["lo"], c["hi"], ns)
+            oracle.prob_array(c["params"], c["L_km"], E, nthreads=nt)
+            u = ns
+        return time.perf_counter() - t0, u
+
+    # size each step to ~ (cpu_seconds / (steps+warmup)), bounded by the workload
+    ns = 2 if args.workload in ("cfg4", "cfg5") else 10_000
+    dt, u = one_step()
+    rate = u / max(dt, 1e-9)
+    per_step = max(0.05, min(args.cpu_seconds, 120.0) / max(args.steps + args.warmup, 1))
+    full = {"cfg4": 10_000, "cfg5": 1000, "cfg2": 100_000, "cfg3": 100_000_000}[args.workload]
+    unit_per = u / ns
+    ns = int(max(1, min(full, rate * per_step / unit_per)))
+    for _ in range(args.warmup):
+        one_step()
+    for _ in range(args.steps):
+        dt, u = one_step()
+        times.append(dt)
+        units.append(u)
+    value = sum(units) / sum(times)
+    sample = "%d of %d %s per step (%s), oracle general complex formula, %d OpenMP threads" % (
+        ns, full, "parameter points" if args.workload in ("cfg4", "cfg5") else
+        ("bins" if args.workload == "cfg2" else "energies"), args.workload, nt)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": c["desc"],
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(c, name, seconds):
+    """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
+    import oracle
+    nt = oracle.max_threads()
+    if name in ("cfg4", "cfg5"):
+        per_point = c["L_km"].size * (c["edges"].size - 1) * c["order"]
+        P = c["points"]["theta12"].size
+        n = 2
+        t0 = time.perf_counter()
+        oracle.batch(synth.subset_points(c["points"], np.arange(n)), c["L_km"], c["omega"],
+                     c["edges"], c["order"], data=c["data"], nthreads=nt)
+        dt = time.perf_counter() - t0
+        n = int(max(1, min(P, seconds / max(dt / n, 1e-9))))
+        idx = np.arange(n)
+        t0 = time.perf_counter()
+        oracle.batch(synth.subset_points(c["points"], idx), c["L_km"], c["omega"], c["edges"],
+                     c["order"], data=c["data"], nthreads=nt)
+        dt = time.perf_counter() - t0
+        units = n * per_point
+        sample = "first %d of %d parameter points of %s (all baselines, bins, nodes)" % (n, P, name)
+    elif name == "cfg2":
+        t0 = time.perf_counter()
+        oracle.gl_integrate(c["params"], c["L_km"], c["edges"], c["order"], nthreads=nt)
+        dt = time.perf_counter() - t0
+        units = (c["edges"].size - 1) * c["order"]
+        sample = "full cfg2"
+    else:
+        n = 20_000_000
+        E = np.linspace(c["lo"], c["hi"], n)
+        t0 = time.perf_counter()
+        oracle.prob_array(c["params"], c["L_km"], E, nthreads=nt)
+        dt = time.perf_counter() - t0
+        units = n
+        sample = "%d of %d energies of cfg3 (same linspace range)" % (n, c["n"])
+    return {"value": units / dt, "unit": UNIT, "cores": nt, "kind": "oracle",
+            "sample": sample, "seconds": dt}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        print("run N>1 under torchrun (WORLD_SIZE unset)", file=sys.stderr)
+        sys.exit(2)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_07682_b200 as gna
+    from paper_1804_07682_b200 import dist as gdist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    gna.load()
+    c = workload(args.workload)
+    f64 = dict(dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    # ---------------- setup (configuration stage): upload once, allocate once
+    if args.workload in ("cfg4", "cfg5"):
+        P = c["points"]["theta12"].size
+        nb = c["edges"].size - 1
+        chunks = args.chunks or (4 if world > 1 else 1)
+        sb = gdist.ShardedBatch(P, nb, world, rank, chunks=chunks).allocate(dev)
+        lo, hi = sb.lo, sb.hi
+        pts = {k: torch.tensor(v[lo:hi], **f64) for k, v in c["points"].items()}
+        edges = torch.tensor(c["edges"], **f64)
+        data = torch.tensor(c["data"], **f64)
+        ws = torch.empty(max(gna.oscprob_batch_workspace_size(max(hi - lo, 1), nb) // 8, 1), **f64)
+        comm = torch.cuda.Stream(device=dev) if world > 1 else None
+        L, om = c["L_km"], c["omega"]
+        kern_ev = []
+
+        def compute(vlo, vhi, sp_rows, x2_rows):
+            sub = {k: v[vlo:vhi] for k, v in pts.items()}
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gna.oscprob_batch(sub, L, om, edges, c["order"], data=data, spectra=sp_rows,
+                              chi2=x2_rows, workspace=ws)
+            e1.record()
+            kern_ev.append((e0, e1))
+
+        def step():
+            sb.step(compute, comm_stream=comm)
+
+        units_per_rank = (hi - lo) * L.size * nb * c["order"]
+        launches_per_step = 2 * len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
+        scaling = "strong"
+    elif args.workload == "cfg2":
+        edges = torch.tensor(c["edges"], **f64)
+        out = torch.empty(c["edges"].size - 1, **f64)
+        kern_ev = []
+
+        def step():
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gna.gl_integrate(c["params"], c["L_km"], edges, c["order"], out=out)
+            e1.record()
+            kern_ev.append((e0, e1))
+
+        units_per_rank = c["evals"]
+        launches_per_step = 1
+        scaling = "weak"  # replicas only
+    else:
+        E = torch.linspace(c["lo"], c["hi"], c["n"], **f64)
+        out = torch.empty_like(E)
+        kern_ev = []
+
+        def step():
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gna.oscprob_eval(c["params"], c["L_km"], E, out=out)
+            e1.record()
+            kern_ev.append((e0, e1))
+
+        units_per_rank = c["evals"]
+        launches_per_step = 1
+        scaling = "weak"  # replicas only
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    # ---------------- warm-up
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    kern_ev.clear()
+
+    # ---------------- timed region: K steps, per-step events, L2 flushed between steps
+    barrier()
+    torch.cuda.synchronize()
+    n_launch0 = gna.launch_count()
+    evs = []
+    with ClockSampler(_smi_index(local)) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            step()
+            s1.record()
+            evs.append((s0, s1))
+        torch.cuda.synchronize()
+    barrier()
+    launches = gna.launch_count() - n_launch0
+    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    kern_ms = [a.elapsed_time(b) for a, b in kern_ev]
+    t = torch.tensor([total_ms, float(np.mean(kern_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_avg_ms = float(t[0]), float(t[1])
+    units_total = units_per_rank if scaling == "strong" else units_per_rank * world
+    if scaling == "strong":
+        units_total = c["evals"]
+    value = units_total * args.steps / (total_ms * 1e-3)
+
+    # ---------------- roofline of the dominant kernel (batch / gl / eval)
+    peak_ops = SM_COUNT * FP64_LANES_PER_SM * (clk.summary()["sm_max_mhz"] or 1965.0) * 1e6
+    if args.workload == "cfg3":
+        # co-limited stream: report the HBM side (16 B per energy) and note FP64
+        launch_units = units_per_rank
+        achieved = launch_units * 16 / (kern_avg_ms * 1e-3) / 1e9
+        peaks = _measured_peaks()
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": peaks["source"],
+                "fp64_frac": launch_units * (FP64_OPS_PER_EVAL + 7) / (kern_avg_ms * 1e-3) / peak_ops}
+    else:
+        launch_units = (units_per_rank / max(launches_per_step // 2, 1)
+                        if args.workload in ("cfg4", "cfg5") else units_per_rank)
+        achieved = launch_units * FP64_OPS_PER_EVAL / (kern_avg_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
+                "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
+                "peak_source": "148 SM x 64 FP64 lanes x sm_max clock (lanes measured by "
+                               "tools/probe_fp64.cu: 18.55 T DFMA/s at 1965 MHz)",
+                "ops_per_energy_point": FP64_OPS_PER_EVAL,
+                "kernel_ms_per_launch": kern_avg_ms}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if scaling == "strong" else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(c["desc"], parallelism="dp%d over parameter points" % world
+                           if scaling == "strong" else "replicas x%d" % world,
+                           l2="flushed between steps (256 MiB write, untimed)",
+                           energy_points_per_step=units_total),
+            "bins_per_s": (c["bins_total"] * args.steps / (total_ms * 1e-3)) if c["bins_total"] else None,
+            "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof}
+
+    # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, c, gna, torch, dist, dev, world, rank, local)
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(c, args.workload, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def _smi_index(local: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    try:
+        return int(vis.split(",")[local]) if vis else local
+    except (ValueError, IndexError):
+        return local
+
+
+def _measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def e2e(args, c, gna, torch, dist, dev, world, rank, local):
+    """Same metric through the host-buffer C ABI: per step H2D of the inputs from pinned
+    memory and D2H of the results (overlapped in chunks inside the library)."""
+    steps = max(args.e2e_steps, 1)
+
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory()
+        return t, t.numpy()
+
+    if args.workload in ("cfg4", "cfg5"):
+        from paper_1804_07682_b200 import dist as gdist
+        P = c["points"]["theta12"].size
+        nb = c["edges"].size - 1
+        lo, hi = gdist.shard_range(P, world, rank)
+        keep = []
+        pts = {}
+        for k, v in c["points"].items():
+            t, a = pinned(v[lo:hi])
+            keep.append(t)
+            pts[k] = a
+        te, edges = pinned(c["edges"])
+        td, data = pinned(c["data"])
+        ts, spectra = pinned(np.empty((hi - lo, nb)))
+        tx, chi2 = pinned(np.empty(hi - lo))
+        keep += [te, td, ts, tx]
+
+        def one():
+            gna.oscprob_batch_host(pts, c["L_km"], c["omega"], edges, c["order"], data=data,
+                                   spectra=spectra, chi2=chi2)
+
+        h2d = 4 * (hi - lo) * 8 + edges.nbytes + data.nbytes
+        d2h = spectra.nbytes + chi2.nbytes
+        units = (hi - lo) * c["L_km"].size * nb * c["order"]
+    elif args.workload == "cfg2":
+        te, edges = pinned(c["edges"])
+        ts, out = pinned(np.empty(c["edges"].size - 1))
+        keep = [te, ts]
+        E_host = None
+
+        def one():
+            # host variant of gl_integrate = H2D edges, kernel, D2H bins
+            d_edges = torch.from_numpy(edges).to(dev, non_blocking=True)
+            b = gna.gl_integrate(c["params"], c["L_km"], d_edges, c["order"])
+            ts.copy_(b, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        h2d, d2h = edges.nbytes, out.nbytes
+        units = c["evals"]
+    else:
+        n = c["n"]
+        tE, E = pinned(np.linspace(c["lo"], c["hi"], n))
+        tP, Pout = pinned(np.empty(n))
+        keep = [tE, tP]
+
+        def one():
+            gna.oscprob_eval_host(c["params"], c["L_km"], E, out=Pout)
+
+        h2d, d2h = E.nbytes, Pout.nbytes
+        units = n
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_units = units * world if args.workload in ("cfg2", "cfg3") else c["evals"]
+    del keep
+    return {"value": total_units * steps / (float(ms[0]) * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "steps": steps, "api": "gna_oscprob_batch_host" if args.workload in ("cfg4", "cfg5")
+            else ("gna_gl_integrate + torch copies" if args.workload == "cfg2"
+                  else "gna_oscprob_eval_host")}
+
+
+if __name__ == "__main__":
+    main()

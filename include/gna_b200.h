@@ -1,0 +1,183 @@
+/*
+ * gna_b200.h — C ABI of the B200-native GNA hot path (libgna_b200.so).
+ *
+ * Source method: arXiv:1804.07682, "GNA: GPU support for the Global Neutrino
+ * Analysis framework".  Citations: P:NNN = reference PAPER.md line NNN (§ given),
+ * S:NNN = reference SPEC.md line NNN, BJ = BASELINE.json north_star, DESIGN.md Rn =
+ * reading n in DESIGN.md.
+ *
+ * What the library computes (all fp64, IEEE binary64, round-to-nearest):
+ *   P_ee(E) — the reactor electron-antineutrino survival probability, the
+ *     alpha = beta = e case of the general vacuum formula P:631-639 (§4.1), with
+ *     Delta_ij = 1.26693268 * dm2_ij[eV^2] * L[km] / (E[MeV] / 1000) (S:265,
+ *     S:317; R1) and dm2_32 = dm2_31 - dm2_21.  For alpha =
+ *     beta = e the formula reduces exactly to
+ *       P_ee = 1 - w21 sin^2 D21 - w31 sin^2 D31 - w32 sin^2 D32,
+ *       w21 = cos^4(t13) sin^2(2 t12), w31 = sin^2(2 t13) cos^2(t12),
+ *       w32 = sin^2(2 t13) sin^2(t12)        (R2),
+ *     so theta23, delta_cp and the antineutrino flag do not change the result.
+ *   Per-bin Gauss-Legendre integrals of P_ee (BJ north_star; R5/R6):
+ *       S_k = h_k * sum_i w_i P_ee(c_k + h_k t_i),
+ *       c_k = (e_k + e_{k+1})/2, h_k = (e_{k+1} - e_k)/2, (t_i, w_i) the n-point
+ *       GL rule on [-1, 1].
+ *   Batched spectra over parameter points and baselines (BJ; the one-energy-
+ *   node / several-OscProb topology of P:596-603 and S:431-439):
+ *       T[p][k] = sum_b omega_b S_{p,b,k},  chi2[p] = sum_k (T[p][k] - D_k)^2 / D_k
+ *       (R8).
+ *
+ * Conventions shared by every entry point
+ *   Ownership: arrays are owned by the caller.  The
+ *     device entry points never allocate, free or synchronise; inputs are read
+ *     only; outputs are fully overwritten.  Input and output ranges must not
+ *     overlap.  The *_host entry points stage through library-owned device
+ *     buffers (grown on first use, released by gna_release()).
+ *   Memory kind: "d_" arrays are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors) of the current device; "h_" arrays are HOST pointers (pinned
+ *     memory gives overlapped copies; pageable memory works, slower).  Scalars
+ *     and small per-call arrays (L_km, omega) are host values.
+ *   Streams: work is enqueued on `stream` (a cudaStream_t; NULL = legacy default
+ *     stream).  Device entry points return after enqueueing: the return code
+ *     covers validation and launch; execution faults surface at the caller's
+ *     next stream synchronisation (adapting P:798-800).  *_host entry points
+ *     return after the results are in host memory.
+ *   Errors: GNA_EINVAL is returned before any CUDA call for bad arguments;
+ *     GNA_ENODEV if the current device is not compute capability 10.0
+ *     (sm_100a); GNA_ECUDA if a CUDA call or launch failed (the cudaError_t is
+ *     then available from gna_last_cuda_error(), thread-local); GNA_ENOMEM if
+ *     staging allocation failed.  Preconditions NOT checked on the device
+ *     (violations give unspecified values, never a fault): E > 0,
+ *     edges strictly increasing, data > 0.
+ *   Domain: phases |Delta| <= 2^40 rad are reduced exactly; the result is
+ *     accurate to the rounding of Delta itself (R7, R9).
+ *   Thread safety: stateless and re-entrant for the device entry points;
+ *     concurrent calls on disjoint outputs are allowed.  The *_host
+ *     entry points serialise on an internal lock per device.
+ */
+#ifndef GNA_B200_H
+#define GNA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNA_ABI_VERSION 1
+#define GNA_MAX_ORDER 32  /* largest Gauss-Legendre order in the table        */
+#define GNA_MAX_NBASE 64  /* largest number of baselines per batch call         */
+
+enum gna_status {
+  GNA_OK = 0,
+  GNA_EINVAL = -1, /* invalid argument (returned before any CUDA call)        */
+  GNA_ECUDA = -2,  /* a CUDA call or kernel launch failed                     */
+  GNA_ENODEV = -3, /* current device is not sm_100 (B200)                     */
+  GNA_ENOMEM = -4  /* library staging allocation failed (*_host only)         */
+};
+
+/* Oscillation parameters — SPEC OscParams.  Angles in radians,
+ * dm2 in eV^2; a negative dm2_31 selects the inverted ordering.
+ * theta23, delta_cp and antineutrino are accepted for interface parity with
+ * the general formula; they do not change P_ee (R2).              */
+typedef struct gna_osc_params {
+  double theta12, theta13, theta23;
+  double delta_cp;
+  double dm2_21, dm2_31;
+  int32_t antineutrino;
+} gna_osc_params;
+
+/* A batch of parameter points, structure of arrays, each [npoints] fp64.
+ * Device pointers for gna_oscprob_batch, host pointers for
+ * gna_oscprob_batch_host.                                                    */
+typedef struct gna_param_batch {
+  const double* theta12;
+  const double* theta13;
+  const double* dm2_21;
+  const double* dm2_31;
+  int64_t npoints;
+} gna_param_batch;
+
+/* ---------------------------------------------------------------------------
+ * gna_oscprob_eval — the OscProb transformation (§4.1, Table 1):
+ *   d_P[i] = P_ee(d_E[i]; L_km, *p)   for 0 <= i < n.
+ * p: host struct (all fields finite).  L_km >= 0, finite.  d_E: device [n]
+ * energies in MeV (> 0).  d_P: device [n] output.  n >= 1.
+ * EINVAL: p/d_E/d_P NULL, n < 1, non-finite scalar, L_km < 0, d_E and d_P
+ * ranges overlap, or a pointer that is not device memory.
+ * ------------------------------------------------------------------------- */
+int gna_oscprob_eval(const gna_osc_params* p, double L_km, const double* d_E, int64_t n,
+                     double* d_P, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * gna_gl_integrate — fused P_ee + per-bin Gauss-Legendre quadrature (BJ):
+ *   d_bins[k] = h_k * sum_{i<order} w_i P_ee(c_k + h_k t_i),  0 <= k < nbins.
+ * d_edges: device [nbins + 1] bin edges in MeV (strictly increasing, > 0).
+ * order in [1, GNA_MAX_ORDER].  d_bins: device [nbins] output.
+ * EINVAL as for gna_oscprob_eval, plus nbins < 1 or order out of range.
+ * ------------------------------------------------------------------------- */
+int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges, int64_t nbins,
+                     int32_t order, double* d_bins, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * gna_oscprob_batch — batch over parameter points x baselines (BJ north_star):
+ *   T[p][k]  = sum_{b<nbase} omega[b] * S_{p,b,k}       -> d_spectra[p*nbins+k]
+ *   chi2[p]  = sum_k (T[p][k] - d_data[k])^2 / d_data[k] -> d_chi2[p]
+ * pts: host struct of DEVICE arrays [npoints] (npoints >= 1).
+ * L_km, omega: HOST arrays [nbase], 1 <= nbase <= GNA_MAX_NBASE, L >= 0.
+ * d_edges: device [nbins + 1].  order in [1, GNA_MAX_ORDER].
+ * d_spectra: device [npoints][nbins] row-major output, or NULL.
+ * d_data: device [nbins] (> 0), required iff d_chi2 != NULL.
+ * d_chi2: device [npoints] output, or NULL (not both outputs NULL).
+ * d_workspace: device scratch of at least
+ *   gna_oscprob_batch_workspace_size(npoints, nbins) bytes when d_chi2 != NULL
+ *   (may be NULL otherwise); contents need no initialisation.
+ * Results are bitwise deterministic and independent of how the points are
+ * split between calls (one point's arithmetic never depends on the others).
+ * ------------------------------------------------------------------------- */
+size_t gna_oscprob_batch_workspace_size(int64_t npoints, int64_t nbins);
+
+int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                      int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                      double* d_spectra, const double* d_data, double* d_chi2,
+                      void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer variants (the end-to-end path; §4.1 "CUDA Streams,
+ * datasets are divided into smaller sizes to organize overlapped execution,
+ * asynchronous memory copying").  Same arithmetic as the device entry points
+ * (bitwise identical results); inputs are copied host->device and results
+ * device->host in chunks so that the copies overlap the kernels.  chunk = 0
+ * picks a default.  Returns after the results are in host memory.
+ * ------------------------------------------------------------------------- */
+int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
+                          double* h_P, int64_t chunk, void* stream);
+
+int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, const double* omega,
+                           int32_t nbase, const double* h_edges, int64_t nbins, int32_t order,
+                           double* h_spectra, const double* h_data, double* h_chi2,
+                           int64_t chunk_points, void* stream);
+
+/* Frees the library-owned staging buffers of the *_host entry points. */
+void gna_release(void);
+
+/* Copies the library's Gauss-Legendre rule of the given order (nodes ascending
+ * on [-1, 1]) into host arrays t[order], w[order].  EINVAL for a bad order.   */
+int gna_gl_rule(int32_t order, double* t, double* w);
+
+/* Human-readable text for a gna_status code (static storage). */
+const char* gna_strerror(int code);
+
+/* cudaError_t behind the last GNA_ECUDA returned on this thread (0 if none). */
+int gna_last_cuda_error(void);
+
+/* GNA_ABI_VERSION of the loaded library. */
+int gna_abi_version(void);
+
+/* Number of kernels launched by this thread through the library since load
+ * (diagnostics for the bench's gpu_launches count).                          */
+int64_t gna_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNA_B200_H */

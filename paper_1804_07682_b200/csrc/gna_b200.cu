@@ -1,0 +1,670 @@
+// gna_b200.cu — sm_100a kernels and the C ABI of libgna_b200.so (include/gna_b200.h).
+//
+// Hot path (BASELINE.json north_star), fp64 throughout:
+//   (a2) per-point coefficients: mixing weights w21/w31/w32 and phase slopes
+//   (a3) P_ee(E) = 1 - sum_ij w_ij sin^2(Delta_ij)            (§4.1)
+//   (a4) S_k = h_k sum_i w_i P_ee(c_k + h_k t_i)                (Gauss-Legendre)
+//   (a5) T[p][k] = sum_b omega_b S_{p,b,k}, chi2[p]             (batch epilogue)
+// Everything after argument validation runs in the kernels below; there is no
+// host or CPU fallback.  See DESIGN.md for the roofline of each kernel.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/gna_b200.h"
+#include "gl_table.h"
+#include "gna_device.cuh"
+
+using gna::PeeCoef;
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// constants
+// ----------------------------------------------------------------------------
+// S:265 / S:317 phase literal (R1); Delta = kPhase * dm2 * L / (E/1000).
+constexpr double kPhase = 1.26693268;
+// 1000 (MeV per GeV) * 2/pi: the kernels work with y = Delta * 2/pi.
+constexpr double kMeV2Over_pi = 636.6197723675813430755;  // 2000/pi
+
+__constant__ double c_gl_t[GNA_GL_TABLE_SIZE] = GNA_GL_NODES_INIT;
+__constant__ double c_gl_w[GNA_GL_TABLE_SIZE] = GNA_GL_WEIGHTS_INIT;
+const double h_gl_t[GNA_GL_TABLE_SIZE] = GNA_GL_NODES_INIT;
+const double h_gl_w[GNA_GL_TABLE_SIZE] = GNA_GL_WEIGHTS_INIT;
+
+std::atomic<int64_t> g_launches{0};
+thread_local int t_last_cuda_error = 0;
+
+constexpr int kEvalThreads = 256;
+constexpr int kGLThreads = 64;
+constexpr int kBatchThreads = 128;
+constexpr int kReduceThreads = 128;
+
+// phase slope in units of pi/2 per 1/MeV: y = kq / E  <=>  Delta = kPhase*dm2*L/(E/1000)
+__host__ __device__ inline double phase_slope(double dm2, double L_km) {
+  return ((kPhase * dm2) * L_km) * kMeV2Over_pi;
+}
+
+// mixing weights of P_ee (R2): w21 = c13^4 sin^2 2t12,
+// w31 = sin^2 2t13 c12^2, w32 = sin^2 2t13 s12^2
+__host__ __device__ inline void mixing_weights(double s12, double c12, double s13, double c13,
+                                               double* w21, double* w31, double* w32) {
+  const double s2t12 = 2.0 * s12 * c12;
+  const double s2t13 = 2.0 * s13 * c13;
+  const double c13sq = c13 * c13;
+  *w21 = (c13sq * c13sq) * (s2t12 * s2t12);
+  *w31 = (s2t13 * s2t13) * (c12 * c12);
+  *w32 = (s2t13 * s2t13) * (s12 * s12);
+}
+
+// ----------------------------------------------------------------------------
+// kernels
+// ----------------------------------------------------------------------------
+
+// (a3) elementwise P_ee, double2-vectorised grid-stride stream.
+template <bool kVec>
+__global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
+                                                               const double* __restrict__ E,
+                                                               double* __restrict__ P, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (kVec) {
+    const int64_t n2 = n >> 1;
+    const double2* __restrict__ E2 = reinterpret_cast<const double2*>(E);
+    double2* __restrict__ P2 = reinterpret_cast<double2*>(P);
+    for (int64_t i = tid; i < n2; i += stride) {
+      const double2 e = __ldcs(E2 + i);
+      double2 r;
+      r.x = gna::pee_inv(c, gna::rcp(e.x));
+      r.y = gna::pee_inv(c, gna::rcp(e.y));
+      __stcs(P2 + i, r);
+    }
+    if ((n & 1) && tid == 0) P[n - 1] = gna::pee_inv(c, gna::rcp(E[n - 1]));
+  } else {
+    for (int64_t i = tid; i < n; i += stride) P[i] = gna::pee_inv(c, gna::rcp(E[i]));
+  }
+}
+
+// (a3)+(a4) one parameter point: one thread per bin, GL nodes from the constant bank.
+__global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int order,
+                                                             const double* __restrict__ edges,
+                                                             int64_t nbins,
+                                                             double* __restrict__ bins) {
+  const int off = GNA_GL_OFF(order);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nbins; k += stride) {
+    const double e0 = edges[k], e1 = edges[k + 1];
+    const double ctr = 0.5 * (e0 + e1);
+    const double h = 0.5 * (e1 - e0);
+    double s = 0.0;
+    for (int i = 0; i < order; ++i) {
+      const double E = fma(h, c_gl_t[off + i], ctr);
+      s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(E)), s);
+    }
+    bins[k] = h * s;
+  }
+}
+
+struct BatchArgs {
+  double L[GNA_MAX_NBASE];
+  double omega[GNA_MAX_NBASE];
+  double omega_sum;  // sum_b omega_b (left to right)
+  int nbase;
+  int order;
+  int64_t nbins;
+  int64_t bpp;  // blocks per point
+};
+
+// deterministic block sum (fixed shuffle tree, then warps in order)
+template <int kThreads>
+__device__ __forceinline__ double block_sum(double x, double* s_warp) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_warp[warp] = x;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; ++w) t += s_warp[w];
+  }
+  return t;
+}
+
+// (a2)+(a3)+(a4)+(a5): block = (parameter point p, tile of kBatchThreads bins).
+__global__ void __launch_bounds__(kBatchThreads) k_oscprob_batch(
+    BatchArgs a, const double* __restrict__ th12, const double* __restrict__ th13,
+    const double* __restrict__ d21, const double* __restrict__ d31,
+    const double* __restrict__ edges, double* __restrict__ spectra,
+    const double* __restrict__ data, double* __restrict__ partial) {
+  __shared__ double2 s_coef[GNA_MAX_NBASE * 3];  // (kq, omega_b * w_ij)
+  __shared__ double s_c0;
+  __shared__ double s_warp[kBatchThreads / 32];
+
+  const int64_t p = blockIdx.x / a.bpp;
+  const int64_t tile = blockIdx.x - p * a.bpp;
+
+  // (a2) per-point coefficients, one thread per baseline
+  if (threadIdx.x < a.nbase) {
+    const int b = threadIdx.x;
+    double s12, c12, s13, c13, w21, w31, w32;
+    sincos(th12[p], &s12, &c12);
+    sincos(th13[p], &s13, &c13);
+    mixing_weights(s12, c12, s13, c13, &w21, &w31, &w32);
+    const double m21 = d21[p], m31 = d31[p];
+    const double m32 = m31 - m21;
+    const double L = a.L[b], om = a.omega[b];
+    s_coef[3 * b + 0] = make_double2(phase_slope(m21, L), om * w21);
+    s_coef[3 * b + 1] = make_double2(phase_slope(m31, L), om * w31);
+    s_coef[3 * b + 2] = make_double2(phase_slope(m32, L), om * w32);
+    if (b == 0) s_c0 = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
+  }
+  __syncthreads();
+
+  const int64_t k = tile * kBatchThreads + threadIdx.x;
+  double x2 = 0.0;
+  if (k < a.nbins) {
+    const int off = GNA_GL_OFF(a.order);
+    const double e0 = edges[k], e1 = edges[k + 1];
+    const double ctr = 0.5 * (e0 + e1);
+    const double h = 0.5 * (e1 - e0);
+    const double c0 = s_c0;
+    const int nterm = 3 * a.nbase;
+    double s = 0.0;
+    for (int i = 0; i < a.order; ++i) {
+      const double invE = gna::rcp(fma(h, c_gl_t[off + i], ctr));
+      double acc = 0.0;
+      for (int j = 0; j < nterm; ++j) {
+        const double2 cw = s_coef[j];
+        acc = gna::sin2c_acc(cw.x * invE, cw.y, acc);
+      }
+      s = fma(c_gl_w[off + i], c0 - acc, s);
+    }
+    const double T = h * s;
+    if (spectra) spectra[p * a.nbins + k] = T;
+    if (data) {
+      const double D = data[k];
+      const double d = T - D;
+      x2 = d * d / D;
+    }
+  }
+  if (partial) {  // uniform branch: chi2 requested
+    const double t = block_sum<kBatchThreads>(x2, s_warp);
+    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+  }
+}
+
+// chi2[p] = sum of the point's tile partials, tiles in order (deterministic)
+__global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
+                                                                int64_t npoints, int64_t bpp,
+                                                                double* __restrict__ chi2) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npoints) return;
+  const double* q = partial + p * bpp;
+  double s = 0.0;
+  for (int64_t j = 0; j < bpp; ++j) s += q[j];
+  chi2[p] = s;
+}
+
+// ----------------------------------------------------------------------------
+// host helpers
+// ----------------------------------------------------------------------------
+int cuda_fail(cudaError_t e) {
+  t_last_cuda_error = (int)e;
+  return GNA_ECUDA;
+}
+
+bool finite(double x) { return std::isfinite(x); }
+
+bool params_ok(const gna_osc_params* p) {
+  return p && finite(p->theta12) && finite(p->theta13) && finite(p->theta23) &&
+         finite(p->delta_cp) && finite(p->dm2_21) && finite(p->dm2_31);
+}
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+  const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+  return x < y + nb && y < x + na;
+}
+
+// 0 ok, else status.  Checks the current device is sm_100 (cached per device).
+int check_device() {
+  static std::atomic<int> state[128];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= 128) return GNA_ENODEV;
+  int s = state[dev].load(std::memory_order_relaxed);
+  if (s == 0) {
+    int major = 0, minor = 0;
+    e = cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    s = (major == 10 && minor == 0) ? 1 : 2;
+    state[dev].store(s, std::memory_order_relaxed);
+  }
+  return s == 1 ? GNA_OK : GNA_ENODEV;
+}
+
+// EINVAL unless ptr is device (or managed) memory.
+int check_dev_ptr(const void* ptr) {
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky-free error
+    return GNA_EINVAL;
+  }
+  return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) ? GNA_OK
+                                                                              : GNA_EINVAL;
+}
+
+void make_coef(const gna_osc_params* p, double L_km, PeeCoef* c) {
+  double w21, w31, w32;
+  mixing_weights(std::sin(p->theta12), std::cos(p->theta12), std::sin(p->theta13),
+                 std::cos(p->theta13), &w21, &w31, &w32);
+  const double m32 = p->dm2_31 - p->dm2_21;
+  c->kq[0] = phase_slope(p->dm2_21, L_km);
+  c->kq[1] = phase_slope(p->dm2_31, L_km);
+  c->kq[2] = phase_slope(m32, L_km);
+  c->w[0] = w21;
+  c->w[1] = w31;
+  c->w[2] = w32;
+  c->c0 = 1.0 - 0.5 * ((w21 + w31) + w32);
+}
+
+int grid_for(int64_t work_items, int threads, int max_blocks) {
+  int64_t b = (work_items + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+int sm_count() {
+  static std::atomic<int> cached{0};
+  int v = cached.load();
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached.store(v);
+  }
+  return v;
+}
+
+// --- validation shared by device and host variants --------------------------
+int validate_eval(const gna_osc_params* p, double L_km, const double* E, int64_t n, const double* P) {
+  if (!params_ok(p) || !E || !P || n < 1 || !finite(L_km) || L_km < 0) return GNA_EINVAL;
+  if (overlap(E, (size_t)n * 8, P, (size_t)n * 8)) return GNA_EINVAL;
+  return GNA_OK;
+}
+
+int validate_gl(const gna_osc_params* p, double L_km, const double* edges, int64_t nbins,
+                int32_t order, const double* bins) {
+  if (!params_ok(p) || !edges || !bins || nbins < 1 || order < 1 || order > GNA_MAX_ORDER ||
+      !finite(L_km) || L_km < 0)
+    return GNA_EINVAL;
+  if (overlap(edges, (size_t)(nbins + 1) * 8, bins, (size_t)nbins * 8)) return GNA_EINVAL;
+  return GNA_OK;
+}
+
+int validate_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                   int32_t nbase, const double* edges, int64_t nbins, int32_t order,
+                   const double* spectra, const double* data, const double* chi2) {
+  if (!pts || !pts->theta12 || !pts->theta13 || !pts->dm2_21 || !pts->dm2_31 ||
+      pts->npoints < 1 || !L_km || !omega || nbase < 1 || nbase > GNA_MAX_NBASE || !edges ||
+      nbins < 1 || order < 1 || order > GNA_MAX_ORDER)
+    return GNA_EINVAL;
+  if (!spectra && !chi2) return GNA_EINVAL;
+  if (chi2 && !data) return GNA_EINVAL;
+  for (int b = 0; b < nbase; ++b)
+    if (!finite(L_km[b]) || L_km[b] < 0 || !finite(omega[b])) return GNA_EINVAL;
+  const size_t P8 = (size_t)pts->npoints * 8;
+  if (spectra) {
+    const size_t S8 = (size_t)pts->npoints * (size_t)nbins * 8;
+    const void* ins[6] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, edges, data};
+    const size_t ln[6] = {P8, P8, P8, P8, (size_t)(nbins + 1) * 8, data ? (size_t)nbins * 8 : 0};
+    for (int i = 0; i < 6; ++i)
+      if (ins[i] && overlap(spectra, S8, ins[i], ln[i])) return GNA_EINVAL;
+    if (chi2 && overlap(spectra, S8, chi2, P8)) return GNA_EINVAL;
+  }
+  if (chi2) {
+    const void* ins[6] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, edges, data};
+    const size_t ln[6] = {P8, P8, P8, P8, (size_t)(nbins + 1) * 8, (size_t)nbins * 8};
+    for (int i = 0; i < 6; ++i)
+      if (overlap(chi2, P8, ins[i], ln[i])) return GNA_EINVAL;
+  }
+  return GNA_OK;
+}
+
+int64_t blocks_per_point(int64_t nbins) { return (nbins + kBatchThreads - 1) / kBatchThreads; }
+
+// launch of the batch kernels on already-validated device arguments
+int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                 int32_t nbase, const double* edges, int64_t nbins, int32_t order,
+                 double* spectra, const double* data, double* chi2, double* partial,
+                 cudaStream_t s) {
+  BatchArgs a;
+  std::memset(&a, 0, sizeof(a));
+  double om = 0.0;
+  for (int b = 0; b < nbase; ++b) {
+    a.L[b] = L_km[b];
+    a.omega[b] = omega[b];
+    om += omega[b];
+  }
+  a.omega_sum = om;
+  a.nbase = nbase;
+  a.order = order;
+  a.nbins = nbins;
+  a.bpp = blocks_per_point(nbins);
+  const int64_t nblocks = pts->npoints * a.bpp;
+  if (nblocks > 0x7fffffffLL) return GNA_EINVAL;
+  k_oscprob_batch<<<(unsigned)nblocks, kBatchThreads, 0, s>>>(
+      a, pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, edges, spectra,
+      chi2 ? data : nullptr, chi2 ? partial : nullptr);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (chi2) {
+    const int grid = (int)((pts->npoints + kReduceThreads - 1) / kReduceThreads);
+    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(partial, pts->npoints, a.bpp, chi2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return GNA_OK;
+}
+
+int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStream_t s) {
+  const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
+  const int maxb = sm_count() * 8;
+  if (vec) {
+    const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);
+    k_oscprob_eval<true><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+  } else {
+    const int grid = grid_for(n, kEvalThreads, maxb);
+    k_oscprob_eval<false><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+
+// ----------------------------------------------------------------------------
+// staging for the *_host entry points (library-owned, per device)
+// ----------------------------------------------------------------------------
+struct Staging {
+  bool init = false;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in = nullptr;
+  void* buf[2] = {nullptr, nullptr};  // per-stream chunk buffers
+  size_t cap[2] = {0, 0};
+  void* shared = nullptr;             // per-call shared inputs (edges, data)
+  size_t shared_cap = 0;
+};
+
+std::mutex g_stage_mu;
+Staging g_stage[128];
+
+int ensure(void** p, size_t* cap, size_t need) {
+  if (*cap >= need) return GNA_OK;
+  if (*p) {
+    cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+  }
+  cudaError_t e = cudaMalloc(p, need);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return GNA_ENOMEM;
+  }
+  *cap = need;
+  return GNA_OK;
+}
+
+int stage_init(Staging* S) {
+  if (S->init) return GNA_OK;
+  cudaError_t e;
+  for (int i = 0; i < 2; ++i) {
+    e = cudaStreamCreateWithFlags(&S->st[i], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  e = cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_fail(e);
+  S->init = true;
+  return GNA_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int gna_oscprob_eval(const gna_osc_params* p, double L_km, const double* d_E, int64_t n,
+                     double* d_P, void* stream) {
+  int rc = validate_eval(p, L_km, d_E, n, d_P);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_E) || check_dev_ptr(d_P)) return GNA_EINVAL;
+  PeeCoef c;
+  make_coef(p, L_km, &c);
+  return launch_eval(c, d_E, n, d_P, (cudaStream_t)stream);
+}
+
+int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges, int64_t nbins,
+                     int32_t order, double* d_bins, void* stream) {
+  int rc = validate_gl(p, L_km, d_edges, nbins, order, d_bins);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
+  PeeCoef c;
+  make_coef(p, L_km, &c);
+  const int grid = grid_for(nbins, kGLThreads, 0x7fffffff);
+  k_gl_integrate<<<grid, kGLThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges, nbins, d_bins);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+
+size_t gna_oscprob_batch_workspace_size(int64_t npoints, int64_t nbins) {
+  if (npoints < 1 || nbins < 1) return 0;
+  return (size_t)npoints * (size_t)blocks_per_point(nbins) * sizeof(double);
+}
+
+int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                      int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                      double* d_spectra, const double* d_data, double* d_chi2,
+                      void* d_workspace, size_t workspace_bytes, void* stream) {
+  int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
+                          d_chi2);
+  if (rc) return rc;
+  if (d_chi2 && (!d_workspace ||
+                 workspace_bytes < gna_oscprob_batch_workspace_size(pts->npoints, nbins)))
+    return GNA_EINVAL;
+  if ((rc = check_device())) return rc;
+  const void* ptrs[9] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, d_edges,
+                         d_spectra,    d_data,       d_chi2,      d_chi2 ? d_workspace : nullptr};
+  for (const void* q : ptrs)
+    if (q && check_dev_ptr(q)) return GNA_EINVAL;
+  return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
+                      (double*)d_workspace, (cudaStream_t)stream);
+}
+
+int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
+                          double* h_P, int64_t chunk, void* stream) {
+  int rc = validate_eval(p, L_km, h_E, n, h_P);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Staging* S = &g_stage[dev];
+  if ((rc = stage_init(S))) return rc;
+  if (chunk <= 0) chunk = (int64_t)1 << 22;  // 4 Mi elements = 32 MiB per direction
+  if (chunk > n) chunk = n;
+  chunk = (chunk + 1) & ~(int64_t)1;         // keep the double2 path aligned
+  const size_t need = (size_t)chunk * 16;    // E and P halves
+  for (int i = 0; i < 2; ++i)
+    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  PeeCoef c;
+  make_coef(p, L_km, &c);
+  cudaError_t e = cudaEventRecord(S->ev_in, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+  int64_t nchunks = (n + chunk - 1) / chunk;
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int si = (int)(ci & 1);
+    cudaStream_t s = S->st[si];
+    const int64_t o = ci * chunk;
+    const int64_t m = (o + chunk <= n) ? chunk : n - o;
+    double* dE = (double*)S->buf[si];
+    double* dP = dE + chunk;
+    if ((e = cudaMemcpyAsync(dE, h_E + o, (size_t)m * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cuda_fail(e);
+    if ((rc = launch_eval(c, dE, m, dP, s))) return rc;
+    if ((e = cudaMemcpyAsync(h_P + o, dP, (size_t)m * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return cuda_fail(e);
+  }
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
+  return GNA_OK;
+}
+
+int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, const double* omega,
+                           int32_t nbase, const double* h_edges, int64_t nbins, int32_t order,
+                           double* h_spectra, const double* h_data, double* h_chi2,
+                           int64_t chunk_points, void* stream) {
+  int rc = validate_batch(h_pts, L_km, omega, nbase, h_edges, nbins, order, h_spectra, h_data,
+                          h_chi2);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Staging* S = &g_stage[dev];
+  if ((rc = stage_init(S))) return rc;
+  const int64_t P = h_pts->npoints;
+  if (chunk_points <= 0) {
+    // ~8 MiB of spectra per chunk, at least 1 point
+    chunk_points = ((int64_t)8 << 20) / (nbins * 8);
+    if (chunk_points < 1) chunk_points = 1;
+  }
+  if (chunk_points > P) chunk_points = P;
+  const int64_t bpp = blocks_per_point(nbins);
+  // per-stream chunk buffer: 4 param arrays + spectra + chi2 + partials
+  const size_t n_par = 4 * (size_t)chunk_points;
+  const size_t n_spec = h_spectra ? (size_t)chunk_points * nbins : 0;
+  const size_t n_chi = h_chi2 ? (size_t)chunk_points : 0;
+  const size_t n_part = h_chi2 ? (size_t)chunk_points * bpp : 0;
+  const size_t need = (n_par + n_spec + n_chi + n_part) * 8;
+  for (int i = 0; i < 2; ++i)
+    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  const size_t n_shared = (size_t)(nbins + 1) + (h_data ? (size_t)nbins : 0);
+  if ((rc = ensure(&S->shared, &S->shared_cap, n_shared * 8))) return rc;
+  double* d_edges = (double*)S->shared;
+  double* d_data = h_data ? d_edges + (nbins + 1) : nullptr;
+
+  cudaError_t e;
+  cudaStream_t s0 = S->st[0];
+  if ((e = cudaEventRecord(S->ev_in, (cudaStream_t)stream)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(s0, S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaMemcpyAsync(d_edges, h_edges, (size_t)(nbins + 1) * 8, cudaMemcpyHostToDevice, s0)))
+    return cuda_fail(e);
+  if (d_data &&
+      (e = cudaMemcpyAsync(d_data, h_data, (size_t)nbins * 8, cudaMemcpyHostToDevice, s0)))
+    return cuda_fail(e);
+  if ((e = cudaEventRecord(S->ev_in, s0)) != cudaSuccess) return cuda_fail(e);
+  if ((e = cudaStreamWaitEvent(S->st[1], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+
+  const double* hsrc[4] = {h_pts->theta12, h_pts->theta13, h_pts->dm2_21, h_pts->dm2_31};
+  const int64_t nchunks = (P + chunk_points - 1) / chunk_points;
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int si = (int)(ci & 1);
+    cudaStream_t s = S->st[si];
+    const int64_t o = ci * chunk_points;
+    const int64_t m = (o + chunk_points <= P) ? chunk_points : P - o;
+    double* base = (double*)S->buf[si];
+    double* dpar = base;
+    double* dspec = h_spectra ? dpar + n_par : nullptr;
+    double* dchi = h_chi2 ? dpar + n_par + n_spec : nullptr;
+    double* dpart = h_chi2 ? dpar + n_par + n_spec + n_chi : nullptr;
+    for (int a = 0; a < 4; ++a)
+      if ((e = cudaMemcpyAsync(dpar + a * chunk_points, hsrc[a] + o, (size_t)m * 8,
+                               cudaMemcpyHostToDevice, s)))
+        return cuda_fail(e);
+    gna_param_batch dp = {dpar, dpar + chunk_points, dpar + 2 * chunk_points,
+                          dpar + 3 * chunk_points, m};
+    if ((rc = launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data, dchi,
+                           dpart, s)))
+      return rc;
+    if (h_spectra && (e = cudaMemcpyAsync(h_spectra + o * nbins, dspec, (size_t)m * nbins * 8,
+                                          cudaMemcpyDeviceToHost, s)))
+      return cuda_fail(e);
+    if (h_chi2 &&
+        (e = cudaMemcpyAsync(h_chi2 + o, dchi, (size_t)m * 8, cudaMemcpyDeviceToHost, s)))
+      return cuda_fail(e);
+  }
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
+  return GNA_OK;
+}
+
+void gna_release(void) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < 128; ++d) {
+    Staging* S = &g_stage[d];
+    if (!S->init && !S->buf[0] && !S->buf[1] && !S->shared) continue;
+    cudaSetDevice(d);
+    for (int i = 0; i < 2; ++i) {
+      if (S->st[i]) cudaStreamSynchronize(S->st[i]);
+      if (S->buf[i]) cudaFree(S->buf[i]);
+      if (S->st[i]) cudaStreamDestroy(S->st[i]);
+      S->buf[i] = nullptr;
+      S->cap[i] = 0;
+      S->st[i] = nullptr;
+    }
+    if (S->shared) cudaFree(S->shared);
+    if (S->ev_in) cudaEventDestroy(S->ev_in);
+    *S = Staging();
+  }
+  cudaSetDevice(cur);
+}
+
+int gna_gl_rule(int32_t order, double* t, double* w) {
+  if (order < 1 || order > GNA_MAX_ORDER || !t || !w) return GNA_EINVAL;
+  const int off = GNA_GL_OFF(order);
+  for (int i = 0; i < order; ++i) {
+    t[i] = h_gl_t[off + i];
+    w[i] = h_gl_w[off + i];
+  }
+  return GNA_OK;
+}
+
+const char* gna_strerror(int code) {
+  switch (code) {
+    case GNA_OK: return "GNA_OK: success";
+    case GNA_EINVAL: return "GNA_EINVAL: invalid argument";
+    case GNA_ECUDA: return "GNA_ECUDA: CUDA call or kernel launch failed (see gna_last_cuda_error)";
+    case GNA_ENODEV: return "GNA_ENODEV: current device is not sm_100 (B200)";
+    case GNA_ENOMEM: return "GNA_ENOMEM: staging allocation failed";
+    default: return "unknown gna_status";
+  }
+}
+
+int gna_last_cuda_error(void) { return t_last_cuda_error; }
+
+int gna_abi_version(void) { return GNA_ABI_VERSION; }
+
+int64_t gna_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

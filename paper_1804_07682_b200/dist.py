@@ -1,0 +1,152 @@
+"""Multi-GPU partition of the batch path.
+
+Parameter points are independent units (§2.3 "divide input data into
+smaller independent datasets"; P:596-603 independent OscProb instances), so
+rank r of G takes the contiguous block [r*P//G, (r+1)*P//G) of points; the
+energy grid, GL rule, baselines and data are replicated (uploaded once per GPU,
+as the paper copies E once).  The only exchange is the gather of the
+per-point binned spectra and chi^2 (BASELINE.json north_star), done with NCCL
+all_gather_into_tensor over NVLink, chunk-pipelined on a communication stream so
+that chunk c's gather overlaps chunk c+1's kernel.
+
+One point's arithmetic never depends on the other points in a call, so the
+gathered result is bitwise identical for every G (tests/test_dist_gloo.py on CPU
+with gloo; tests/test_gpu_parity.py split invariance on the GPU).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+
+def shard_range(npoints: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced block of points owned by `rank` (counts differ by <= 1)."""
+    if world < 1 or not 0 <= rank < world or npoints < 0:
+        raise ValueError("bad shard request")
+    return rank * npoints // world, (rank + 1) * npoints // world
+
+
+def padded_rows(npoints: int, world: int) -> int:
+    """Rows per rank in the gathered layout (all_gather needs equal sizes)."""
+    return -(-npoints // world)
+
+
+def chunk_bounds(rows: int, chunks: int) -> list[tuple[int, int]]:
+    chunks = max(1, min(chunks, max(rows, 1)))
+    return [(c * rows // chunks, (c + 1) * rows // chunks) for c in range(chunks)]
+
+
+def gather_index(npoints: int, world: int, chunks: int = 1) -> np.ndarray:
+    """Position of global point p in the gathered, padded, chunk-major buffer.
+
+    Gathered layout: for chunk c (bounds over the padded row count Pl), a block
+    [world, rows_c] — i.e. element (c, r, i) holds local row lo_c + i of rank r.
+    """
+    Pl = padded_rows(npoints, world)
+    cb = chunk_bounds(Pl, chunks)
+    pos = np.empty(npoints, dtype=np.int64)
+    base = 0
+    starts = []
+    for lo, hi in cb:
+        starts.append(base)
+        base += world * (hi - lo)
+    for r in range(world):
+        a, b = shard_range(npoints, world, r)
+        for j in range(b - a):
+            c = next(k for k, (lo, hi) in enumerate(cb) if lo <= j < hi)
+            lo, hi = cb[c]
+            pos[a + j] = starts[c] + r * (hi - lo) + (j - lo)
+    return pos
+
+
+@dataclass
+class ShardedBatch:
+    """Per-rank state of the sharded batch step (spectra + chi^2, gathered on every rank).
+
+    compute(lo, hi, spectra_rows, chi2_rows) fills the local rows [lo, hi) of the
+    rank's shard; by default it is the CUDA path (gna.oscprob_batch) — tests on
+    CPU pass the oracle instead to exercise the partition and gather logic
+    with gloo.
+    """
+    npoints: int
+    nbins: int
+    world: int
+    rank: int
+    chunks: int = 1
+    group: object = None
+
+    def __post_init__(self):
+        self.lo, self.hi = shard_range(self.npoints, self.world, self.rank)
+        self.count = self.hi - self.lo
+        self.Pl = padded_rows(self.npoints, self.world)
+        self.cb = chunk_bounds(self.Pl, self.chunks)
+
+    def allocate(self, device, want_spectra=True, want_chi2=True):
+        import torch
+        f64 = dict(dtype=torch.float64, device=device)
+        self.spectra = torch.zeros((self.Pl, self.nbins), **f64) if want_spectra else None
+        self.chi2 = torch.zeros(self.Pl, **f64) if want_chi2 else None
+        # chunk-major gathered buffers: chunk c -> [world, rows_c, ...]
+        self.g_spectra = ([torch.empty((self.world, hi - lo, self.nbins), **f64)
+                           for lo, hi in self.cb] if want_spectra else None)
+        self.g_chi2 = ([torch.empty((self.world, hi - lo), **f64) for lo, hi in self.cb]
+                       if want_chi2 else None)
+        return self
+
+    def step(self, compute: Callable, comm_stream=None):
+        """Compute every chunk, gathering chunk c while chunk c+1 computes."""
+        import torch
+        import torch.distributed as dist
+        works = []
+        on_cuda = self.spectra is not None and self.spectra.is_cuda or (
+            self.chi2 is not None and self.chi2.is_cuda)
+        for c, (lo, hi) in enumerate(self.cb):
+            vlo, vhi = min(lo, self.count), min(hi, self.count)  # valid rows of this chunk
+            if vhi > vlo:
+                compute(vlo, vhi,
+                        self.spectra[vlo:vhi] if self.spectra is not None else None,
+                        self.chi2[vlo:vhi] if self.chi2 is not None else None)
+            if self.world == 1:
+                continue
+            if on_cuda and comm_stream is not None:
+                ev = torch.cuda.Event()
+                ev.record()
+                with torch.cuda.stream(comm_stream):
+                    comm_stream.wait_event(ev)
+                    works += self._gather_chunk(c, lo, hi, dist)
+            else:
+                works += self._gather_chunk(c, lo, hi, dist)
+        for w in works:
+            w.wait()
+        if on_cuda and comm_stream is not None and self.world > 1:
+            torch.cuda.current_stream().wait_stream(comm_stream)
+
+    def _gather_chunk(self, c, lo, hi, dist):
+        ws = []
+        if self.spectra is not None:
+            ws.append(dist.all_gather_into_tensor(self.g_spectra[c], self.spectra[lo:hi],
+                                                  group=self.group, async_op=True))
+        if self.chi2 is not None:
+            ws.append(dist.all_gather_into_tensor(self.g_chi2[c], self.chi2[lo:hi],
+                                                  group=self.group, async_op=True))
+        return ws
+
+    def gathered(self):
+        """(spectra [P, nbins], chi2 [P]) in global point order (copies; for checks)."""
+        import torch
+        if self.world == 1:
+            s = self.spectra[:self.count] if self.spectra is not None else None
+            x = self.chi2[:self.count] if self.chi2 is not None else None
+            return s, x
+        pos = torch.as_tensor(gather_index(self.npoints, self.world, len(self.cb)),
+                              device=(self.spectra if self.spectra is not None else self.chi2).device)
+        s = x = None
+        if self.spectra is not None:
+            flat = torch.cat([g.reshape(-1, self.nbins) for g in self.g_spectra])
+            s = flat.index_select(0, pos)
+        if self.chi2 is not None:
+            flat = torch.cat([g.reshape(-1) for g in self.g_chi2])
+            x = flat.index_select(0, pos)
+        return s, x

@@ -1,0 +1,193 @@
+"""CPU-side checks of the C-ABI library (no GPU needed).
+
+* libgna_b200.so loads and exports every function include/gna_b200.h declares;
+* every invalid-argument path returns GNA_EINVAL before any CUDA call;
+* the library's Gauss-Legendre table equals an independent rule (oracle
+  Newton and numpy leggauss);
+* the sin^2 polynomial of the kernels meets its accuracy claim when evaluated
+  exactly as the kernel does (fp64 FMA Horner, emulated with Fractions).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+from fractions import Fraction
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+import paper_1804_07682_b200 as gna
+from paper_1804_07682_b200 import _build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "gna_b200.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return gna.load()
+
+
+def _declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gna_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    declared = _declared_functions()
+    assert len(declared) >= 10
+    assert sorted(declared) == sorted(gna.EXPORTS)
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert ctypes.cast(getattr(lib, name), ctypes.c_void_p).value
+
+
+def test_sm100a_only_cubin(lib):
+    # the fatbin carries sm_100a SASS and no other architecture
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _build.LIB], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_strerror_and_version(lib):
+    assert gna.abi_version() == 1
+    for code in (0, -1, -2, -3, -4):
+        assert lib.gna_strerror(code).startswith(b"GNA_")
+    assert lib.gna_strerror(7) == b"unknown gna_status"
+    assert lib.gna_last_cuda_error() == 0
+
+
+BAD = ctypes.c_void_p(0x10000)    # non-null fake addresses: validation must reject
+BAD2 = ctypes.c_void_p(0x900000)  # before touching them
+
+
+def _params(**kw):
+    p = gna.OscParams(**kw)._c()
+    return ctypes.byref(p)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=0), dict(n=-5), dict(E=None), dict(P=None), dict(L=-1.0), dict(L=float("nan")),
+    dict(L=float("inf")), dict(theta12=float("nan")), dict(dm2_31=float("inf")),
+    dict(P=ctypes.c_void_p(0x10000 + 8)),  # overlaps E
+])
+def test_eval_einval(lib, case):
+    n = case.get("n", 100)
+    E = case.get("E", BAD)
+    P = case.get("P", BAD2)
+    L = case.get("L", 52.5)
+    pk = {k: v for k, v in case.items() if k in ("theta12", "dm2_31")}
+    for f in (lambda: lib.gna_oscprob_eval(_params(**pk), L, E, n, P, None),
+              lambda: lib.gna_oscprob_eval_host(_params(**pk), L, E, n, P, 0, None)):
+        assert f() == gna.GNA_EINVAL
+
+
+def test_eval_null_params(lib):
+    assert lib.gna_oscprob_eval(None, 1.0, BAD, 10, BAD2, None) == gna.GNA_EINVAL
+
+
+@pytest.mark.parametrize("case", [
+    dict(nbins=0), dict(order=0), dict(order=33), dict(edges=None), dict(bins=None),
+    dict(L=-0.5), dict(bins=ctypes.c_void_p(0x10000 + 16)),
+])
+def test_gl_einval(lib, case):
+    r = lib.gna_gl_integrate(_params(), case.get("L", 52.5), case.get("edges", BAD),
+                             case.get("nbins", 10), case.get("order", 5), case.get("bins", BAD2),
+                             None)
+    assert r == gna.GNA_EINVAL
+
+
+def _batch(lib, host=False, **kw):
+    P = kw.get("npoints", 4)
+    pts = gna._CBatch(0x100000, 0x200000, 0x300000, kw.get("d31", 0x400000), P)
+    nb = kw.get("nbase", 2)
+    L = np.asarray(kw.get("L", [52.5, 1.0][:max(nb, 0)] + [1.0] * max(nb - 2, 0)), dtype=float)
+    om = np.ones(max(nb, 1))
+    if L.size < max(nb, 1):
+        L = np.resize(L, max(nb, 1))
+    args = [ctypes.byref(pts), L.ctypes.data, om.ctypes.data, nb, kw.get("edges", 0x500000),
+            kw.get("nbins", 10), kw.get("order", 5), kw.get("spectra", 0x600000),
+            kw.get("data", 0x700000), kw.get("chi2", 0x800000)]
+    if host:
+        return lib.gna_oscprob_batch_host(*args, 0, None)
+    return lib.gna_oscprob_batch(*args, kw.get("ws", 0x900000), kw.get("wsb", 1 << 20), None)
+
+
+@pytest.mark.parametrize("case", [
+    dict(npoints=0), dict(nbase=0), dict(nbase=65), dict(nbins=0), dict(order=0),
+    dict(order=33), dict(spectra=None, chi2=None), dict(data=None), dict(edges=None),
+    dict(d31=None), dict(L=[52.5, -1.0]), dict(L=[float("nan"), 1.0]),
+    dict(chi2=0x600000 + 8),          # chi2 inside spectra
+    dict(spectra=0x100000 - 8),       # spectra overlaps theta12
+    dict(ws=None), dict(wsb=8),       # chi2 requested without enough workspace
+])
+def test_batch_einval(lib, case):
+    assert _batch(lib, **case) == gna.GNA_EINVAL
+    if "ws" not in case and "wsb" not in case:
+        assert _batch(lib, host=True, **case) == gna.GNA_EINVAL
+
+
+def test_batch_workspace_size(lib):
+    assert gna.oscprob_batch_workspace_size(0, 10) == 0
+    assert gna.oscprob_batch_workspace_size(10, 0) == 0
+    ws = gna.oscprob_batch_workspace_size(1000, 10_000)
+    assert ws >= 1000 * 8 and ws % 8 == 0
+
+
+def test_valid_call_without_gpu_does_not_crash(lib):
+    # on the CPU box there is no device: a valid call reports ECUDA/ENODEV/EINVAL, never crashes
+    r = lib.gna_oscprob_eval(_params(), 52.5, BAD, 10, BAD2, None)
+    assert r in (gna.GNA_ECUDA, gna.GNA_ENODEV, gna.GNA_EINVAL, gna.GNA_OK)
+
+
+@pytest.mark.parametrize("n", list(range(1, 33)))
+def test_library_gl_rule_matches_independent_rules(lib, n):
+    t, w = gna.gl_rule(n)
+    to, wo = oracle.gauleg(n)
+    tn, wn = np.polynomial.legendre.leggauss(n)
+    assert np.max(np.abs(t - to)) <= 2.3e-16 and np.max(np.abs(w - wo)) <= 4.5e-16
+    assert np.max(np.abs(t - tn)) <= 4e-16 and np.max(np.abs(w - wn)) <= 6e-15
+    assert np.array_equal(t, -t[::-1])
+
+
+def test_gl_rule_einval(lib):
+    buf = np.zeros(40)
+    assert lib.gna_gl_rule(0, buf.ctypes.data, buf.ctypes.data) == gna.GNA_EINVAL
+    assert lib.gna_gl_rule(33, buf.ctypes.data, buf.ctypes.data) == gna.GNA_EINVAL
+
+
+def _sin2_coeffs():
+    src = open(os.path.join(_build.CSRC, "sin2_poly.h")).read()
+    cs = dict(re.findall(r"#define GNA_SIN2_C(\d) \(([-0-9a-fx.p+]+)\)", src))
+    return [float.fromhex(cs[str(j)]) for j in range(len(cs))]
+
+
+def _fma(a, b, c):
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def test_kernel_sin2_polynomial_accuracy():
+    """sin^2((pi/2)(q+f)) = 1/2 + (-1)^q V(f^2) with the kernel's fp64 Horner: |err| <= 1.2e-16."""
+    cf = _sin2_coeffs()
+    assert len(cf) == 9 and cf[0] == -0.5
+    mp.mp.dps = 40
+    g = np.random.default_rng(3)
+    fs = np.r_[np.linspace(-0.5, 0.5, 801), g.uniform(-0.5, 0.5, 400)]
+    worst = 0.0
+    for f in fs:
+        u = float(f) * float(f)
+        p = cf[-1]
+        for c in reversed(cf[:-1]):
+            p = _fma(p, u, c)
+        for q in (0, 1, 7, 100):
+            got = 0.5 + (p if q % 2 == 0 else -p)
+            ref = mp.sin(mp.pi / 2 * (q + mp.mpf(float(f)))) ** 2
+            worst = max(worst, abs(float(got - ref)))
+    assert worst <= 1.2e-16 + 1.2e-16  # polynomial + final half-ulp of 1/2 +- v

@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star; R7): 1e-12 absolute on
+probabilities, 1e-11 relative on bin integrals and spectra; chi^2 within the
+bound that the 1e-11 spectra tolerance propagates to.  Inputs are the seeded
+synthetic workloads of synth/ (DESIGN.md "Input recipe").  Run on a B200 via
+gpurun: python -m pytest tests -m gpu
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_P = 1e-12
+TOL_BIN = 1e-11
+EPS = np.finfo(np.float64).eps
+
+
+@pytest.fixture(scope="module")
+def gna():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1804_07682_b200 import _build
+    _build.build()
+    import paper_1804_07682_b200 as g
+    g.load()
+    torch.cuda.set_device(0)
+    return g
+
+
+def _t(a):
+    import torch
+    return torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+
+
+def _np(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def _nt():
+    return oracle.max_threads()
+
+
+def _chi2_bound(T, D):
+    d = np.abs(T - D)
+    return np.sum((2 * d * TOL_BIN * np.abs(T) + d * d * 8 * EPS) / D, axis=-1) + 1e-300
+
+
+# ------------------------------------------------------------------------ (a3) eval
+def test_eval_cfg1(gna):
+    c = synth.config("cfg1")
+    P = _np(gna.oscprob_eval(c["params"], c["L_km"], _t(c["E"])))
+    Pr = oracle.prob_array(c["params"], c["L_km"], c["E"])
+    assert np.max(np.abs(P - Pr)) <= TOL_P
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 257, 1000, 4097, 100_003])
+def test_eval_random_params_ragged(gna, n):
+    g = synth.rng(100 + n)
+    for _ in range(6):
+        p = synth.random_params(g)
+        L = g.uniform(0, 300)
+        E = synth.random_energies(g, n)
+        P = _np(gna.oscprob_eval(p, L, _t(E)))
+        Pr = oracle.prob_array(p, L, E, nthreads=_nt())
+        assert np.max(np.abs(P - Pr)) <= TOL_P, (p, L)
+
+
+def test_eval_misaligned_scalar_path(gna):
+    import torch
+    g = synth.rng(7)
+    E = synth.random_energies(g, 1001)
+    buf = _t(np.r_[0.0, E])
+    Ein = buf[1:]                      # 8-byte aligned only -> scalar kernel
+    out = torch.empty(1002, dtype=torch.float64, device="cuda")[1:]
+    p = dict(synth.CANONICAL)
+    P = _np(gna.oscprob_eval(p, 52.5, Ein, out=out))
+    assert np.max(np.abs(P - oracle.prob_array(p, 52.5, E))) <= TOL_P
+
+
+def test_eval_special_cases(gna):
+    E = np.linspace(1, 10, 999)
+    p0 = dict(synth.CANONICAL, theta12=0.0, theta13=0.0)
+    assert np.all(_np(gna.oscprob_eval(p0, 52.5, _t(E))) == 1.0)       # zero mixing
+    P = _np(gna.oscprob_eval(synth.CANONICAL, 0.0, _t(E)))             # L = 0
+    assert np.max(np.abs(P - 1.0)) <= 2 * EPS
+    # theta13 = 0: two-flavour limit via the oracle's two_flavor
+    p1 = dict(synth.CANONICAL, theta13=0.0)
+    P = _np(gna.oscprob_eval(p1, 52.5, _t(E)))
+    ref = np.array([oracle.two_flavor(p1["theta12"], p1["dm2_21"], 52.5, e) for e in E])
+    assert np.max(np.abs(P - ref)) <= TOL_P
+    # theta23, delta, antineutrino do not change P_ee (R2): bitwise
+    pa = dict(synth.CANONICAL, theta23=0.1, delta_cp=2.0, antineutrino=1)
+    assert np.array_equal(_np(gna.oscprob_eval(pa, 52.5, _t(E))),
+                          _np(gna.oscprob_eval(synth.CANONICAL, 52.5, _t(E))))
+
+
+def test_eval_stress_domain_within_conditioning_bound(gna):
+    # angles over [0, pi/2], L up to 300 km: agreement within the rounding bound
+    # of the phases (R7): sum_ij w_ij |2 Delta_ij| * 8 eps
+    g = synth.rng(9)
+    for _ in range(10):
+        p = synth.random_params(g, domain=dict(synth.PARITY_DOMAIN, theta12=(0, np.pi / 2),
+                                               theta13=(0, np.pi / 2)))
+        L = g.uniform(0, 300)
+        E = synth.random_energies(g, 20_000)
+        P = _np(gna.oscprob_eval(p, L, _t(E)))
+        Pr = oracle.prob_array(p, L, E, nthreads=_nt())
+        dm = np.array([p["dm2_21"], p["dm2_31"], p["dm2_31"] - p["dm2_21"]])
+        ph = np.abs(1.26693268 * dm[:, None] * L / (E[None, :] / 1000.0))
+        bound = 1e-15 + np.sum(2 * ph * 8 * EPS, axis=0)  # w_ij <= 1
+        assert np.all(np.abs(P - Pr) <= bound)
+
+
+def test_eval_cfg3_full_size_sampled(gna):
+    """cfg3: 1e8 energies streamed from HBM, as bench.py launches it; sampled parity."""
+    import torch
+    c = synth.config("cfg3")
+    E = torch.linspace(c["lo"], c["hi"], c["n"], dtype=torch.float64, device="cuda")
+    P = gna.oscprob_eval(c["params"], c["L_km"], E)
+    idx = np.r_[0:64, synth.rng(3).integers(0, c["n"], 10_000), c["n"] - 64:c["n"]]
+    it = torch.tensor(idx, device="cuda")
+    Es, Ps = _np(E[it]), _np(P[it])
+    Pr = oracle.prob_array(c["params"], c["L_km"], Es)
+    assert np.max(np.abs(Ps - Pr)) <= TOL_P
+    assert float(P.min()) >= 0.0 and float(P.max()) <= 1.0 + TOL_P
+    del E, P
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------------ (a4) GL
+def test_gl_cfg1(gna):
+    c = synth.config("cfg1")
+    S = _np(gna.gl_integrate(c["params"], c["L_km"], _t(c["edges"]), c["order"]))
+    Sr = oracle.gl_integrate(c["params"], c["L_km"], c["edges"], c["order"])
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
+
+
+def test_gl_cfg2_full(gna):
+    c = synth.config("cfg2")
+    S = _np(gna.gl_integrate(c["params"], c["L_km"], _t(c["edges"]), c["order"]))
+    Sr = oracle.gl_integrate(c["params"], c["L_km"], c["edges"], c["order"], nthreads=_nt())
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
+
+
+@pytest.mark.parametrize("order", list(range(1, 33)))
+def test_gl_all_orders(gna, order):
+    g = synth.rng(200 + order)
+    p = synth.random_params(g)
+    L = g.uniform(1, 300)
+    edges = np.sort(g.uniform(1.0, 10.0, 38))
+    S = _np(gna.gl_integrate(p, L, _t(edges), order))
+    Sr = oracle.gl_integrate(p, L, edges, order)
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
+
+
+@pytest.mark.parametrize("nbins", [1, 63, 64, 65, 1000, 100_003])
+def test_gl_ragged_sizes(gna, nbins):
+    g = synth.rng(300 + nbins)
+    p = synth.random_params(g)
+    edges = synth.uniform_edges(nbins, 1.0, 10.0)
+    S = _np(gna.gl_integrate(p, 52.5, _t(edges), 7))
+    Sr = oracle.gl_integrate(p, 52.5, edges, 7, nthreads=_nt())
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
+
+
+def test_gl_zero_mixing_is_bin_width(gna):
+    e = synth.uniform_edges(333, 1.0, 10.0)
+    p0 = dict(synth.CANONICAL, theta12=0.0, theta13=0.0)
+    S = _np(gna.gl_integrate(p0, 52.5, _t(e), 10))
+    assert np.max(np.abs(S / np.diff(e) - 1)) <= 4 * EPS
+
+
+# ------------------------------------------------------------------------ (a5) batch
+def _batch_case(g, P, nbase, nbins, order):
+    pts = synth.points_uniform(g, P, dict(theta12=(0.5, 0.65), theta13=(0.1, 0.2),
+                                          dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+    L = g.uniform(1.0, 300.0, nbase)
+    om = g.uniform(0.1, 2.0, nbase)
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    data = synth.pseudo_data(g, edges, om.sum())
+    return pts, L, om, edges, data
+
+
+def _run_batch(gna, pts, L, om, edges, order, data, spectra=True):
+    sp, x2 = gna.oscprob_batch({k: _t(v) for k, v in pts.items()}, L, om, _t(edges), order,
+                               data=_t(data) if data is not None else None, spectra=spectra)
+    return (_np(sp) if sp is not None else None), (_np(x2) if x2 is not None else None)
+
+
+@pytest.mark.parametrize("P,nbase,nbins,order", [
+    (7, 3, 37, 4), (1, 1, 1, 1), (3, 2, 128, 10), (5, 8, 129, 10), (2, 64, 50, 32),
+    (33, 1, 300, 5)])
+def test_batch_small_vs_oracle(gna, P, nbase, nbins, order):
+    g = synth.rng(400 + P * nbase + nbins)
+    pts, L, om, edges, data = _batch_case(g, P, nbase, nbins, order)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data)
+    spr, x2r = oracle.batch(pts, L, om, edges, order, data=data, nthreads=_nt())
+    assert np.max(np.abs(sp - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2 - x2r) <= _chi2_bound(spr, data))
+    # chi2-only and spectra-only runs give the same bits
+    sp2, _ = _run_batch(gna, pts, L, om, edges, order, None)
+    _, x22 = _run_batch(gna, pts, L, om, edges, order, data, spectra=False)
+    assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
+
+
+def test_batch_single_baseline_matches_gl_integrate(gna):
+    g = synth.rng(41)
+    pts, _, _, edges, _ = _batch_case(g, 4, 1, 200, 10)
+    sp, _ = _run_batch(gna, pts, [52.5], [1.0], edges, 10, None)
+    for p in range(4):
+        pp = dict(synth.CANONICAL, **{k: float(v[p]) for k, v in pts.items()})
+        S = _np(gna.gl_integrate(pp, 52.5, _t(edges), 10))
+        assert np.max(np.abs(sp[p] - S) / S) <= 1e-14
+
+
+def _check_sampled(sp, x2, c, idx):
+    sub = synth.subset_points(c["points"], idx)
+    spr, x2r = oracle.batch(sub, c["L_km"], c["omega"], c["edges"], c["order"], data=c["data"],
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, c["data"]))
+
+
+def test_batch_cfg4_full_size_sampled(gna):
+    c = synth.config("cfg4")
+    sp, x2 = _run_batch(gna, c["points"], c["L_km"], c["omega"], c["edges"], c["order"],
+                        c["data"])
+    assert sp.shape == (10_000, 1000) and np.all(np.isfinite(sp)) and np.all(x2 >= 0)
+    _check_sampled(sp, x2, c, np.r_[0, 1, synth.rng(4).integers(0, 10_000, 6), 9999])
+
+
+def test_batch_cfg5_full_size_sampled_and_split_invariant(gna):
+    c = synth.config("cfg5")
+    sp, x2 = _run_batch(gna, c["points"], c["L_km"], c["omega"], c["edges"], c["order"],
+                        c["data"])
+    assert sp.shape == (1000, 10_000) and np.all(np.isfinite(sp)) and np.all(x2 >= 0)
+    _check_sampled(sp, x2, c, np.array([0, 417, 999]))
+    # deterministic, and a point's result does not depend on the other points
+    # in the call (the multi-GPU shard property)
+    sp_b, x2_b = _run_batch(gna, c["points"], c["L_km"], c["omega"], c["edges"], c["order"],
+                            c["data"])
+    assert np.array_equal(sp, sp_b) and np.array_equal(x2, x2_b)
+    for lo, hi in ((0, 125), (125, 563), (563, 1000)):
+        sub = synth.subset_points(c["points"], np.arange(lo, hi))
+        sps, x2s = _run_batch(gna, sub, c["L_km"], c["omega"], c["edges"], c["order"],
+                              c["data"])
+        assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi])
+
+
+# ------------------------------------------------------------------------ host-buffer path
+def test_eval_host_bitwise_equals_device(gna):
+    g = synth.rng(51)
+    E = synth.random_energies(g, 1_000_003)
+    p = synth.random_params(g)
+    Ph = gna.oscprob_eval_host(p, 80.0, E, chunk=65_536)
+    Pd = _np(gna.oscprob_eval(p, 80.0, _t(E)))
+    assert np.array_equal(Ph, Pd)
+
+
+def test_batch_host_bitwise_equals_device(gna):
+    g = synth.rng(52)
+    pts, L, om, edges, data = _batch_case(g, 11, 3, 257, 6)
+    sph, x2h = gna.oscprob_batch_host(pts, L, om, edges, 6, data=data, chunk_points=3)
+    spd, x2d = _run_batch(gna, pts, L, om, edges, 6, data)
+    assert np.array_equal(sph, spd) and np.array_equal(x2h, x2d)
+    _, x2h2 = gna.oscprob_batch_host(pts, L, om, edges, 6, data=data, spectra=False)
+    assert np.array_equal(x2h2, x2d)
+
+
+# ------------------------------------------------------------------------ ABI on the GPU
+def test_host_pointer_to_device_entry_is_einval(gna):
+    import ctypes
+    E = np.linspace(1, 10, 100)
+    P = np.empty(100)
+    p = gna.OscParams()._c()
+    rc = gna.load().gna_oscprob_eval(ctypes.byref(p), 52.5, E.ctypes.data, 100, P.ctypes.data,
+                                     None)
+    assert rc == gna.GNA_EINVAL
+
+
+def test_launch_count_increments(gna):
+    n0 = gna.launch_count()
+    gna.gl_integrate(synth.CANONICAL, 52.5, _t(synth.uniform_edges(10)), 5)
+    assert gna.launch_count() == n0 + 1
