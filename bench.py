@@ -170,7 +170,7 @@ def run_reference(args, rank, world):
         return time.perf_counter() - t0, u
 
     # size each step to ~ (cpu_seconds / (steps+warmup)), bounded by the workload
-    ns = 2 if args.workload in ("cfg4", "cfg5") else 10_000
+    ns = nt if args.workload in ("cfg4", "cfg5") else 10_000
     dt, u = one_step()
     rate = u / max(dt, 1e-9)
     per_step = max(0.05, min(args.cpu_seconds, 120.0) / max(args.steps + args.warmup, 1))
@@ -206,12 +206,12 @@ def cpu_baseline(c, name, seconds):
     if name in ("cfg4", "cfg5"):
         per_point = c["L_km"].size * (c["edges"].size - 1) * c["order"]
         P = c["points"]["theta12"].size
-        n = 2
+        n = min(P, nt)  # calibrate with one point per thread (the oracle threads over points)
         t0 = time.perf_counter()
         oracle.batch(synth.subset_points(c["points"], np.arange(n)), c["L_km"], c["omega"],
                      c["edges"], c["order"], data=c["data"], nthreads=nt)
         dt = time.perf_counter() - t0
-        n = int(max(1, min(P, seconds / max(dt / n, 1e-9))))
+        n = int(max(1, min(P, nt * round(seconds / max(dt, 1e-9)))))
         idx = np.arange(n)
         t0 = time.perf_counter()
         oracle.batch(synth.subset_points(c["points"], idx), c["L_km"], c["omega"], c["edges"],
@@ -276,7 +276,8 @@ def main():
         pts = {k: torch.tensor(v[lo:hi], **f64) for k, v in c["points"].items()}
         edges = torch.tensor(c["edges"], **f64)
         data = torch.tensor(c["data"], **f64)
-        ws = torch.empty(max(gna.oscprob_batch_workspace_size(max(hi - lo, 1), nb) // 8, 1), **f64)
+        ws = torch.empty(max(gna.oscprob_batch_workspace_size(
+            max(hi - lo, 1), c["L_km"].size, nb, c["order"]) // 8, 2), **f64)
         comm = torch.cuda.Stream(device=dev) if world > 1 else None
         L, om = c["L_km"], c["omega"]
         kern_ev = []

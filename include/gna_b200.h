@@ -128,13 +128,16 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
  * d_spectra: device [npoints][nbins] row-major output, or NULL.
  * d_data: device [nbins] (> 0), required iff d_chi2 != NULL.
  * d_chi2: device [npoints] output, or NULL (not both outputs NULL).
- * d_workspace: device scratch of at least
- *   gna_oscprob_batch_workspace_size(npoints, nbins) bytes when d_chi2 != NULL
- *   (may be NULL otherwise); contents need no initialisation.
+ * d_workspace: device scratch, 16-byte aligned, of at least
+ *   gna_oscprob_batch_workspace_size(npoints, nbase, nbins, order) bytes (always
+ *   required: it holds the per-point coefficients, the per-node 1/E and h*w
+ *   tables and the chi2 partials); contents need no initialisation and are
+ *   overwritten; it must not overlap any other argument.
  * Results are bitwise deterministic and independent of how the points are
  * split between calls (one point's arithmetic never depends on the others).
  * ------------------------------------------------------------------------- */
-size_t gna_oscprob_batch_workspace_size(int64_t npoints, int64_t nbins);
+size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t nbins,
+                                        int32_t order);  /* 0 for invalid sizes */
 
 int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
                       int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
@@ -173,7 +176,7 @@ int gna_last_cuda_error(void);
 /* GNA_ABI_VERSION of the loaded library. */
 int gna_abi_version(void);
 
-/* Number of kernels launched by this thread through the library since load
+/* Number of kernels launched through the library (all threads) since load
  * (diagnostics for the bench's gpu_launches count).                          */
 int64_t gna_launch_count(void);
 

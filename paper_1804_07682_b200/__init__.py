@@ -103,7 +103,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     B = ctypes.POINTER(_CBatch)
     L.gna_oscprob_eval.argtypes = [P, d, vp, i64, vp, vp]
     L.gna_gl_integrate.argtypes = [P, d, vp, i64, i32, vp, vp]
-    L.gna_oscprob_batch_workspace_size.argtypes = [i64, i64]
+    L.gna_oscprob_batch_workspace_size.argtypes = [i64, i32, i64, i32]
     L.gna_oscprob_batch_workspace_size.restype = sz
     L.gna_oscprob_batch.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
     L.gna_oscprob_eval_host.argtypes = [P, d, vp, i64, vp, i64, vp]
@@ -191,8 +191,9 @@ def gl_integrate(params, L_km: float, edges, order: int, out=None, stream=None):
     return out
 
 
-def oscprob_batch_workspace_size(npoints: int, nbins: int) -> int:
-    return int(load().gna_oscprob_batch_workspace_size(int(npoints), int(nbins)))
+def oscprob_batch_workspace_size(npoints: int, nbase: int, nbins: int, order: int) -> int:
+    return int(load().gna_oscprob_batch_workspace_size(int(npoints), int(nbase), int(nbins),
+                                                       int(order)))
 
 
 def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spectra=True,
@@ -215,13 +216,11 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
         spectra = None
     if data is not None and chi2 is None:
         chi2 = torch.empty(P, dtype=torch.float64, device=dev)
-    ws_bytes = 0
-    if chi2 is not None:
-        ws_bytes = oscprob_batch_workspace_size(P, nbins)
-        if workspace is None:
-            workspace = torch.empty(max(ws_bytes // 8, 1), dtype=torch.float64, device=dev)
-    b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
     Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    if workspace is None:
+        ws_bytes = oscprob_batch_workspace_size(P, Lh.size, nbins, order)
+        workspace = torch.empty(max(ws_bytes // 8, 2), dtype=torch.float64, device=dev)
+    b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
     if Lh.size != om.size:
         raise ValueError("L_km and omega must have the same length")
     _check(L.gna_oscprob_batch(
@@ -229,8 +228,7 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
         int(order), _dev(spectra, "spectra", P * nbins) if spectra is not None else None,
         _dev(data, "data", nbins) if data is not None else None,
         _dev(chi2, "chi2", P) if chi2 is not None else None,
-        _dev(workspace, "workspace") if workspace is not None else None,
-        workspace.numel() * 8 if workspace is not None else 0, _stream(stream)),
+        _dev(workspace, "workspace"), workspace.numel() * 8, _stream(stream)),
         "gna_oscprob_batch")
     return spectra, chi2
 

@@ -41,8 +41,10 @@ thread_local int t_last_cuda_error = 0;
 
 constexpr int kEvalThreads = 256;
 constexpr int kGLThreads = 64;
-constexpr int kBatchThreads = 128;
+constexpr int kBatchWarps = 4;
 constexpr int kReduceThreads = 128;
+
+__device__ __forceinline__ int64_t warps_per_point_dev(int64_t nbins) { return (nbins + 31) / 32; }
 
 // phase slope in units of pi/2 per 1/MeV: y = kq / E  <=>  Delta = kPhase*dm2*L/(E/1000)
 __host__ __device__ inline double phase_slope(double dm2, double L_km) {
@@ -109,48 +111,68 @@ __global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int orde
   }
 }
 
-struct BatchArgs {
+struct BatchSetupArgs {
   double L[GNA_MAX_NBASE];
   double omega[GNA_MAX_NBASE];
   double omega_sum;  // sum_b omega_b (left to right)
   int nbase;
   int order;
   int64_t nbins;
-  int64_t bpp;  // blocks per point
+  int64_t npoints;
 };
 
-// deterministic block sum (fixed shuffle tree, then warps in order)
-template <int kThreads>
-__device__ __forceinline__ double block_sum(double x, double* s_warp) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) s_warp[warp] = x;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; ++w) t += s_warp[w];
-  }
-  return t;
+// Workspace layout of the batch path (all offsets 16-byte aligned), see
+// gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
+// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp].
+struct BatchWs {
+  double2* coef;
+  double* c0;
+  double* invE;
+  double* hw;
+  double* partial;
+};
+
+size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+int64_t warps_per_point(int64_t nbins) { return (nbins + 31) / 32; }
+
+size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
+  size_t b = align16((size_t)P * nbase * 3 * sizeof(double2));
+  b += align16((size_t)P * sizeof(double));
+  b += 2 * align16((size_t)order * nbins * sizeof(double));
+  if (chi2) b += align16((size_t)P * warps_per_point(nbins) * sizeof(double));
+  return b;
 }
 
-// (a2)+(a3)+(a4)+(a5): block = (parameter point p, tile of kBatchThreads bins).
-__global__ void __launch_bounds__(kBatchThreads) k_oscprob_batch(
-    BatchArgs a, const double* __restrict__ th12, const double* __restrict__ th13,
-    const double* __restrict__ d21, const double* __restrict__ d31,
-    const double* __restrict__ edges, double* __restrict__ spectra,
-    const double* __restrict__ data, double* __restrict__ partial) {
-  __shared__ double2 s_coef[GNA_MAX_NBASE * 3];  // (kq, omega_b * w_ij)
-  __shared__ double s_c0;
-  __shared__ double s_warp[kBatchThreads / 32];
+BatchWs batch_ws_carve(void* base, int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
+  char* c = (char*)base;
+  BatchWs w;
+  w.coef = (double2*)c;
+  c += align16((size_t)P * nbase * 3 * sizeof(double2));
+  w.c0 = (double*)c;
+  c += align16((size_t)P * sizeof(double));
+  w.invE = (double*)c;
+  c += align16((size_t)order * nbins * sizeof(double));
+  w.hw = (double*)c;
+  c += align16((size_t)order * nbins * sizeof(double));
+  w.partial = chi2 ? (double*)c : nullptr;
+  return w;
+}
 
-  const int64_t p = blockIdx.x / a.bpp;
-  const int64_t tile = blockIdx.x - p * a.bpp;
-
-  // (a2) per-point coefficients, one thread per baseline
-  if (threadIdx.x < a.nbase) {
-    const int b = threadIdx.x;
+// (a1)+(a2) setup: per-(point, baseline) coefficients and the per-node tables
+//   invE[i][k] = 1 / (c_k + h_k t_i),  hw[i][k] = h_k w_i   (shared by every point).
+__global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
+                                                     const double* __restrict__ th12,
+                                                     const double* __restrict__ th13,
+                                                     const double* __restrict__ d21,
+                                                     const double* __restrict__ d31,
+                                                     const double* __restrict__ edges, BatchWs w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = a.npoints * a.nbase;
+  const int64_t n2 = (int64_t)a.order * a.nbins;
+  if (t < n1) {
+    const int64_t p = t / a.nbase;
+    const int b = (int)(t - p * a.nbase);
     double s12, c12, s13, c13, w21, w31, w32;
     sincos(th12[p], &s12, &c12);
     sincos(th13[p], &s13, &c13);
@@ -158,56 +180,103 @@ __global__ void __launch_bounds__(kBatchThreads) k_oscprob_batch(
     const double m21 = d21[p], m31 = d31[p];
     const double m32 = m31 - m21;
     const double L = a.L[b], om = a.omega[b];
-    s_coef[3 * b + 0] = make_double2(phase_slope(m21, L), om * w21);
-    s_coef[3 * b + 1] = make_double2(phase_slope(m31, L), om * w31);
-    s_coef[3 * b + 2] = make_double2(phase_slope(m32, L), om * w32);
-    if (b == 0) s_c0 = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
-  }
-  __syncthreads();
-
-  const int64_t k = tile * kBatchThreads + threadIdx.x;
-  double x2 = 0.0;
-  if (k < a.nbins) {
+    double2* c = w.coef + t * 3;
+    c[0] = make_double2(phase_slope(m21, L), om * w21);
+    c[1] = make_double2(phase_slope(m31, L), om * w31);
+    c[2] = make_double2(phase_slope(m32, L), om * w32);
+    if (b == 0) w.c0[p] = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
+  } else if (t < n1 + n2) {
+    const int64_t idx = t - n1;
+    const int i = (int)(idx / a.nbins);
+    const int64_t k = idx - (int64_t)i * a.nbins;
     const int off = GNA_GL_OFF(a.order);
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
     const double h = 0.5 * (e1 - e0);
-    const double c0 = s_c0;
-    const int nterm = 3 * a.nbase;
-    double s = 0.0;
-    for (int i = 0; i < a.order; ++i) {
-      const double invE = gna::rcp(fma(h, c_gl_t[off + i], ctr));
-      double acc = 0.0;
-      for (int j = 0; j < nterm; ++j) {
-        const double2 cw = s_coef[j];
-        acc = gna::sin2c_acc(cw.x * invE, cw.y, acc);
-      }
-      s = fma(c_gl_w[off + i], c0 - acc, s);
-    }
-    const double T = h * s;
-    if (spectra) spectra[p * a.nbins + k] = T;
-    if (data) {
-      const double D = data[k];
-      const double d = T - D;
-      x2 = d * d / D;
-    }
-  }
-  if (partial) {  // uniform branch: chi2 requested
-    const double t = block_sum<kBatchThreads>(x2, s_warp);
-    if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    w.invE[idx] = 1.0 / fma(h, c_gl_t[off + i], ctr);
+    w.hw[idx] = h * c_gl_w[off + i];
   }
 }
 
-// chi2[p] = sum of the point's tile partials, tiles in order (deterministic)
-__global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
-                                                                int64_t npoints, int64_t bpp,
-                                                                double* __restrict__ chi2) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= npoints) return;
-  const double* q = partial + p * bpp;
+// (a3)+(a4)+(a5) main pass.  Block = (point p, kBatchWarps x 32 bins); every warp
+// is independent (no block barrier): it copies its point's coefficient row into
+// a warp-private smem slice, then each lane integrates one bin, two GL nodes at a
+// time so each (kq, w) load feeds two sin^2 evaluations.
+template <int kWarps>
+__global__ void __launch_bounds__(kWarps * 32) k_oscprob_batch(
+    int nterm, int order, int64_t nbins, int64_t bpp, BatchWs w,
+    double* __restrict__ spectra, const double* __restrict__ data) {
+  extern __shared__ double2 s_coef[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p = blockIdx.x / bpp;
+  const int64_t wt = (blockIdx.x - p * bpp) * kWarps + warp;  // warp tile within the point
+  const int64_t k0 = wt * 32;
+  if (k0 >= nbins) return;  // whole warp
+  double2* sc = s_coef + warp * nterm;
+  const double2* __restrict__ gc = w.coef + p * nterm;
+  for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
+  __syncwarp();
+
+  const int64_t k = k0 + lane;
+  const bool active = k < nbins;
+  const int64_t kk = active ? k : nbins - 1;
+  const double c0 = w.c0[p];
+  const double* __restrict__ invE = w.invE + kk;
+  const double* __restrict__ hw = w.hw + kk;
   double s = 0.0;
-  for (int64_t j = 0; j < bpp; ++j) s += q[j];
-  chi2[p] = s;
+  int i = 0;
+  for (; i + 1 < order; i += 2) {
+    const double iE0 = invE[(int64_t)i * nbins], iE1 = invE[(int64_t)(i + 1) * nbins];
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < nterm; ++j) {
+      const double2 cw = sc[j];
+      a0 = fma(cw.y, gna::sin2c(cw.x, iE0), a0);
+      a1 = fma(cw.y, gna::sin2c(cw.x, iE1), a1);
+    }
+    s = fma(hw[(int64_t)i * nbins], c0 - a0, s);
+    s = fma(hw[(int64_t)(i + 1) * nbins], c0 - a1, s);
+  }
+  if (i < order) {
+    const double iE0 = invE[(int64_t)i * nbins];
+    double a0 = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < nterm; ++j) {
+      const double2 cw = sc[j];
+      a0 = fma(cw.y, gna::sin2c(cw.x, iE0), a0);
+    }
+    s = fma(hw[(int64_t)i * nbins], c0 - a0, s);
+  }
+  double x2 = 0.0;
+  if (active) {
+    if (spectra) spectra[p * nbins + k] = s;
+    if (data) {
+      const double D = data[k];
+      const double d = s - D;
+      x2 = d * d / D;
+    }
+  }
+  if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+    if (lane == 0) w.partial[p * warps_per_point_dev(nbins) + wt] = x2;
+  }
+}
+
+// chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
+// in order, then a fixed xor tree (deterministic, independent of scheduling).
+__global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
+                                                                int64_t npoints, int64_t wpp,
+                                                                double* __restrict__ chi2) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= npoints) return;
+  const double* q = partial + p * wpp;
+  double s = 0.0;
+  for (int64_t j = lane; j < wpp; j += 32) s += q[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) chi2[p] = s;
 }
 
 // ----------------------------------------------------------------------------
@@ -341,14 +410,16 @@ int validate_batch(const gna_param_batch* pts, const double* L_km, const double*
   return GNA_OK;
 }
 
-int64_t blocks_per_point(int64_t nbins) { return (nbins + kBatchThreads - 1) / kBatchThreads; }
+int64_t blocks_per_point(int64_t nbins) {
+  return (warps_per_point(nbins) + kBatchWarps - 1) / kBatchWarps;
+}
 
 // launch of the batch kernels on already-validated device arguments
 int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
                  int32_t nbase, const double* edges, int64_t nbins, int32_t order,
-                 double* spectra, const double* data, double* chi2, double* partial,
+                 double* spectra, const double* data, double* chi2, void* workspace,
                  cudaStream_t s) {
-  BatchArgs a;
+  BatchSetupArgs a;
   std::memset(&a, 0, sizeof(a));
   double om = 0.0;
   for (int b = 0; b < nbase; ++b) {
@@ -360,18 +431,31 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
   a.nbase = nbase;
   a.order = order;
   a.nbins = nbins;
-  a.bpp = blocks_per_point(nbins);
-  const int64_t nblocks = pts->npoints * a.bpp;
-  if (nblocks > 0x7fffffffLL) return GNA_EINVAL;
-  k_oscprob_batch<<<(unsigned)nblocks, kBatchThreads, 0, s>>>(
-      a, pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, edges, spectra,
-      chi2 ? data : nullptr, chi2 ? partial : nullptr);
+  a.npoints = pts->npoints;
+  const BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
+  const int64_t bpp = blocks_per_point(nbins);
+  const int64_t nblocks = pts->npoints * bpp;
+  const int64_t nsetup = pts->npoints * nbase + (int64_t)order * nbins;
+  if (nblocks > 0x7fffffffLL || (nsetup + 255) / 256 > 0x7fffffffLL) return GNA_EINVAL;
+
+  k_batch_setup<<<(unsigned)((nsetup + 255) / 256), 256, 0, s>>>(
+      a, pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, edges, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
+
+  const int nterm = 3 * nbase;
+  const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
+  k_oscprob_batch<kBatchWarps><<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
+      nterm, order, nbins, bpp, w, spectra, chi2 ? data : nullptr);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
   if (chi2) {
-    const int grid = (int)((pts->npoints + kReduceThreads - 1) / kReduceThreads);
-    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(partial, pts->npoints, a.bpp, chi2);
+    const int64_t threads = pts->npoints * 32;
+    const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
+    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints, warps_per_point(nbins),
+                                                  chi2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
@@ -473,9 +557,12 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
 
-size_t gna_oscprob_batch_workspace_size(int64_t npoints, int64_t nbins) {
-  if (npoints < 1 || nbins < 1) return 0;
-  return (size_t)npoints * (size_t)blocks_per_point(nbins) * sizeof(double);
+size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t nbins,
+                                        int32_t order) {
+  if (npoints < 1 || nbins < 1 || nbase < 1 || nbase > GNA_MAX_NBASE || order < 1 ||
+      order > GNA_MAX_ORDER)
+    return 0;
+  return batch_ws_bytes(npoints, nbase, nbins, order, true);
 }
 
 int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
@@ -485,16 +572,27 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
   int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
                           d_chi2);
   if (rc) return rc;
-  if (d_chi2 && (!d_workspace ||
-                 workspace_bytes < gna_oscprob_batch_workspace_size(pts->npoints, nbins)))
+  if (!d_workspace ||
+      workspace_bytes < batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr) ||
+      ((uintptr_t)d_workspace & 15))
     return GNA_EINVAL;
+  {
+    const size_t W = batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr);
+    const size_t P8 = (size_t)pts->npoints * 8;
+    const void* ins[8] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31,
+                          d_edges,      d_spectra,    d_data,     d_chi2};
+    const size_t ln[8] = {P8, P8, P8, P8, (size_t)(nbins + 1) * 8,
+                          (size_t)pts->npoints * (size_t)nbins * 8, (size_t)nbins * 8, P8};
+    for (int i = 0; i < 8; ++i)
+      if (ins[i] && overlap(d_workspace, W, ins[i], ln[i])) return GNA_EINVAL;
+  }
   if ((rc = check_device())) return rc;
   const void* ptrs[9] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, d_edges,
-                         d_spectra,    d_data,       d_chi2,      d_chi2 ? d_workspace : nullptr};
+                         d_spectra,    d_data,       d_chi2,      d_workspace};
   for (const void* q : ptrs)
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
-                      (double*)d_workspace, (cudaStream_t)stream);
+                      d_workspace, (cudaStream_t)stream);
 }
 
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
@@ -558,13 +656,13 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
     if (chunk_points < 1) chunk_points = 1;
   }
   if (chunk_points > P) chunk_points = P;
-  const int64_t bpp = blocks_per_point(nbins);
-  // per-stream chunk buffer: 4 param arrays + spectra + chi2 + partials
+  // per-stream chunk buffer: workspace (16-aligned, first) + 4 param arrays + spectra + chi2
+  const size_t ws_bytes = batch_ws_bytes(chunk_points, nbase, nbins, order, h_chi2 != nullptr);
+  const size_t n_ws = ws_bytes / 8;
   const size_t n_par = 4 * (size_t)chunk_points;
   const size_t n_spec = h_spectra ? (size_t)chunk_points * nbins : 0;
   const size_t n_chi = h_chi2 ? (size_t)chunk_points : 0;
-  const size_t n_part = h_chi2 ? (size_t)chunk_points * bpp : 0;
-  const size_t need = (n_par + n_spec + n_chi + n_part) * 8;
+  const size_t need = (n_ws + n_par + n_spec + n_chi) * 8;
   for (int i = 0; i < 2; ++i)
     if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
   const size_t n_shared = (size_t)(nbins + 1) + (h_data ? (size_t)nbins : 0);
@@ -592,10 +690,10 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
     const int64_t o = ci * chunk_points;
     const int64_t m = (o + chunk_points <= P) ? chunk_points : P - o;
     double* base = (double*)S->buf[si];
-    double* dpar = base;
+    void* dws = base;
+    double* dpar = base + n_ws;
     double* dspec = h_spectra ? dpar + n_par : nullptr;
     double* dchi = h_chi2 ? dpar + n_par + n_spec : nullptr;
-    double* dpart = h_chi2 ? dpar + n_par + n_spec + n_chi : nullptr;
     for (int a = 0; a < 4; ++a)
       if ((e = cudaMemcpyAsync(dpar + a * chunk_points, hsrc[a] + o, (size_t)m * 8,
                                cudaMemcpyHostToDevice, s)))
@@ -603,7 +701,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
     gna_param_batch dp = {dpar, dpar + chunk_points, dpar + 2 * chunk_points,
                           dpar + 3 * chunk_points, m};
     if ((rc = launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data, dchi,
-                           dpart, s)))
+                           dws, s)))
       return rc;
     if (h_spectra && (e = cudaMemcpyAsync(h_spectra + o * nbins, dspec, (size_t)m * nbins * 8,
                                           cudaMemcpyDeviceToHost, s)))

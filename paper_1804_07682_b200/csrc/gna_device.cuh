@@ -1,16 +1,16 @@
 // gna_device.cuh — device building blocks of the fused P_ee / GL path (sm_100a, fp64).
 //
 // Arithmetic per sin^2 term, all on the FP64 pipe:
-//   y  = kq * invE          DMUL   (kq = 1.26693268*dm2*L*1000 * 2/pi, so Delta = (pi/2) y)
-//   t  = y + 1.5*2^52       DADD   (rounds y to the nearest integer q, held in t's low word)
-//   q  = t - 1.5*2^52       DADD   (exact)
-//   f  = y - q              DADD   (exact, |f| <= 1/2)
-//   u  = f * f              DMUL
-//   v  = V(u)               8 DFMA (minimax, |err| <= 1.1e-16; sin2_poly.h)
-//   acc += (-1)^q w v       DFMA   (sign applied to w with 2 integer ops on the hi word)
-// = 14 FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
-// v(f) = -cos(pi f)/2.  The reduction is exact for |y| < 2^51, so the only error
-// beyond the polynomial's is the rounding of y itself (R7, R9).
+//   t  = kq * invE + 1.5*2^52   DFMA  (rounds y = kq/E to the nearest integer q, in t's low word)
+//   q  = t - 1.5*2^52           DADD  (exact)
+//   f  = kq * invE - q          DFMA  (one rounding of the exact product minus q, |f| <= 1/2)
+//   u  = f * f                  DMUL
+//   v  = V(u)                   8 DFMA (minimax, |err| <= 1.1e-16; sin2_poly.h)
+//   acc += w * ((-1)^q v)       DFMA  (sign of v flipped with 2 integer ops on its hi word)
+// = 13 FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
+// v(f) = -cos(pi f)/2, so that sum_ij w_ij sin^2 = sum w_ij / 2 + sum w_ij (-1)^q v.
+// The reduction is exact for |y| < 2^51; the only error beyond the polynomial's is
+// the rounding of kq and invE (R7, R9).
 #pragma once
 #include <cstdint>
 
@@ -20,25 +20,28 @@ namespace gna {
 
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 
-// (-1)^q * v(f) * w  accumulated into acc, for y = q + f.
-__device__ __forceinline__ double sin2c_acc(double y, double w, double acc) {
-  const double t = y + kRoundMagic;
+// minimax coefficients in the constant bank: DFMA takes c[][] operands directly,
+// so the Horner chain needs no register or uniform-register moves.
+__constant__ double c_sin2[9] = {GNA_SIN2_C0, GNA_SIN2_C1, GNA_SIN2_C2, GNA_SIN2_C3, GNA_SIN2_C4,
+                                 GNA_SIN2_C5, GNA_SIN2_C6, GNA_SIN2_C7, GNA_SIN2_C8};
+
+// (-1)^q * V(f^2) for y = kq * invE = q + f  (y itself is never rounded separately)
+__device__ __forceinline__ double sin2c(double kq, double invE) {
+  const double t = fma(kq, invE, kRoundMagic);
   const double q = t - kRoundMagic;
-  const double f = y - q;
+  const double f = fma(kq, invE, -q);
   const double u = f * f;
-  double p = GNA_SIN2_C8;
-  p = fma(p, u, GNA_SIN2_C7);
-  p = fma(p, u, GNA_SIN2_C6);
-  p = fma(p, u, GNA_SIN2_C5);
-  p = fma(p, u, GNA_SIN2_C4);
-  p = fma(p, u, GNA_SIN2_C3);
-  p = fma(p, u, GNA_SIN2_C2);
-  p = fma(p, u, GNA_SIN2_C1);
-  p = fma(p, u, GNA_SIN2_C0);
-  // parity of q = bit 0 of t's low word; flip the sign of w when q is odd
-  const uint32_t odd = static_cast<uint32_t>(__double2loint(t)) << 31;
-  const double ws = __hiloint2double(__double2hiint(w) ^ static_cast<int>(odd), __double2loint(w));
-  return fma(ws, p, acc);
+  double p = fma(u, c_sin2[8], c_sin2[7]);
+  p = fma(p, u, c_sin2[6]);
+  p = fma(p, u, c_sin2[5]);
+  p = fma(p, u, c_sin2[4]);
+  p = fma(p, u, c_sin2[3]);
+  p = fma(p, u, c_sin2[2]);
+  p = fma(p, u, c_sin2[1]);
+  p = fma(p, u, c_sin2[0]);
+  // parity of q = bit 0 of t's low word -> sign bit of p
+  const int odd = __double2loint(t) << 31;
+  return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
 }
 
 // 1/x for x > 0 (normal): MUFU.RCP64H seed + two Newton steps (4 DFMA).
@@ -60,9 +63,9 @@ struct PeeCoef {
 };
 
 __device__ __forceinline__ double pee_inv(const PeeCoef& c, double invE) {
-  double acc = sin2c_acc(c.kq[0] * invE, c.w[0], 0.0);
-  acc = sin2c_acc(c.kq[1] * invE, c.w[1], acc);
-  acc = sin2c_acc(c.kq[2] * invE, c.w[2], acc);
+  double acc = c.w[0] * sin2c(c.kq[0], invE);
+  acc = fma(c.w[1], sin2c(c.kq[1], invE), acc);
+  acc = fma(c.w[2], sin2c(c.kq[2], invE), acc);
   return c.c0 - acc;
 }
 

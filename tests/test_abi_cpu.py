@@ -126,7 +126,9 @@ def _batch(lib, host=False, **kw):
     dict(d31=None), dict(L=[52.5, -1.0]), dict(L=[float("nan"), 1.0]),
     dict(chi2=0x600000 + 8),          # chi2 inside spectra
     dict(spectra=0x100000 - 8),       # spectra overlaps theta12
-    dict(ws=None), dict(wsb=8),       # chi2 requested without enough workspace
+    dict(ws=None), dict(wsb=8),       # workspace missing or too small
+    dict(ws=0x900008),                # workspace not 16-byte aligned
+    dict(ws=0x100000 - 64),           # workspace overlaps theta12
 ])
 def test_batch_einval(lib, case):
     assert _batch(lib, **case) == gna.GNA_EINVAL
@@ -135,10 +137,15 @@ def test_batch_einval(lib, case):
 
 
 def test_batch_workspace_size(lib):
-    assert gna.oscprob_batch_workspace_size(0, 10) == 0
-    assert gna.oscprob_batch_workspace_size(10, 0) == 0
-    ws = gna.oscprob_batch_workspace_size(1000, 10_000)
-    assert ws >= 1000 * 8 and ws % 8 == 0
+    assert gna.oscprob_batch_workspace_size(0, 1, 10, 5) == 0
+    assert gna.oscprob_batch_workspace_size(10, 1, 0, 5) == 0
+    assert gna.oscprob_batch_workspace_size(10, 0, 10, 5) == 0
+    assert gna.oscprob_batch_workspace_size(10, 65, 10, 5) == 0
+    assert gna.oscprob_batch_workspace_size(10, 1, 10, 33) == 0
+    ws = gna.oscprob_batch_workspace_size(1000, 8, 10_000, 10)
+    # coefficients + c0 + two node tables + chi2 partials
+    assert ws >= 1000 * 8 * 3 * 16 + 1000 * 8 + 2 * 10 * 10_000 * 8 + 1000 * 313 * 8
+    assert ws % 16 == 0
 
 
 def test_valid_call_without_gpu_does_not_crash(lib):
