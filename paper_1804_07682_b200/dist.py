@@ -41,8 +41,9 @@ def chunk_bounds(rows: int, chunks: int) -> list[tuple[int, int]]:
 def gather_index(npoints: int, world: int, chunks: int = 1) -> np.ndarray:
     """Position of global point p in the gathered, padded, chunk-major buffer.
 
-    Gathered layout: for chunk c (bounds over the padded row count Pl), a block
-    [world, rows_c] — i.e. element (c, r, i) holds local row lo_c + i of rank r.
+    Gathered layout: for chunk c (bounds over the padded row count Pl), a block of
+    world * rows_c rows, rank-major — row r * rows_c + i of chunk c holds local
+    row lo_c + i of rank r.
     """
     Pl = padded_rows(npoints, world)
     cb = chunk_bounds(Pl, chunks)
@@ -88,10 +89,10 @@ class ShardedBatch:
         f64 = dict(dtype=torch.float64, device=device)
         self.spectra = torch.zeros((self.Pl, self.nbins), **f64) if want_spectra else None
         self.chi2 = torch.zeros(self.Pl, **f64) if want_chi2 else None
-        # chunk-major gathered buffers: chunk c -> [world, rows_c, ...]
-        self.g_spectra = ([torch.empty((self.world, hi - lo, self.nbins), **f64)
+        # chunk-major gathered buffers: chunk c -> [world * rows_c, ...] (rank-major rows)
+        self.g_spectra = ([torch.empty((self.world * (hi - lo), self.nbins), **f64)
                            for lo, hi in self.cb] if want_spectra else None)
-        self.g_chi2 = ([torch.empty((self.world, hi - lo), **f64) for lo, hi in self.cb]
+        self.g_chi2 = ([torch.empty(self.world * (hi - lo), **f64) for lo, hi in self.cb]
                        if want_chi2 else None)
         return self
 

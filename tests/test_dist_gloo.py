@@ -1,0 +1,111 @@
+"""Multi-process (world_size 2 and 3) CPU tests of the parameter-point partition and
+the chunk-pipelined gather (paper_1804_07682_b200/dist.py), on the gloo backend.
+
+The compute step is the oracle on each rank's shard (the CUDA path runs on one
+GPU only in this environment); the partition, padding, chunking, collective and
+unpadding logic is exactly the code bench.py runs over NCCL.  The gathered
+result must be bitwise identical to the single-process oracle on all points.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_1804_07682_b200 import dist as gdist
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case(P=11, nbins=13, nbase=2, order=4):
+    g = synth.rng(77)
+    pts = synth.points_uniform(g, P, dict(theta12=(0.5, 0.65), theta13=(0.1, 0.2),
+                                          dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+    L = np.array([52.5, 215.0][:nbase])
+    om = np.array([1.0, 0.1][:nbase])
+    edges = synth.uniform_edges(nbins, 1.0, 10.0)
+    data = synth.pseudo_data(g, edges, om.sum())
+    return pts, L, om, edges, order, data
+
+
+def _worker(rank, world, port, chunks, P, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pts, L, om, edges, order, data = _case(P=P)
+        nb = edges.size - 1
+        sb = gdist.ShardedBatch(P, nb, world, rank, chunks=chunks).allocate("cpu")
+
+        def compute(vlo, vhi, sp_rows, x2_rows):
+            idx = np.arange(sb.lo + vlo, sb.lo + vhi)
+            sp, x2 = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data)
+            sp_rows.copy_(torch.from_numpy(sp))
+            x2_rows.copy_(torch.from_numpy(x2))
+
+        sb.step(compute)
+        s, x = sb.gathered()
+        out_q.put((rank, s.numpy().copy(), x.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,chunks,P", [(2, 1, 11), (2, 3, 11), (3, 2, 7), (2, 2, 1)])
+def test_sharded_gather_bitwise_equals_single_process(world, chunks, P):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, chunks, P, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pts, L, om, edges, order, data = _case(P=P)
+    sp, x2 = oracle.batch(pts, L, om, edges, order, data=data)
+    for rank, s, x in res:
+        assert np.array_equal(s, sp), rank  # every rank holds the full, ordered result
+        assert np.array_equal(x, x2), rank
+
+
+@pytest.mark.parametrize("P,world", [(0, 1), (1, 1), (7, 2), (1000, 8), (1001, 8), (5, 8)])
+def test_shard_range_partitions(P, world):
+    cover = []
+    counts = []
+    for r in range(world):
+        lo, hi = gdist.shard_range(P, world, r)
+        cover += list(range(lo, hi))
+        counts.append(hi - lo)
+    assert cover == list(range(P))
+    assert max(counts) - min(counts) <= 1
+    assert max(counts) <= gdist.padded_rows(P, world)
+
+
+@pytest.mark.parametrize("P,world,chunks", [(11, 2, 1), (11, 2, 3), (7, 3, 2), (1000, 8, 4),
+                                            (3, 8, 2)])
+def test_gather_index_is_injective_into_padded_layout(P, world, chunks):
+    pos = gdist.gather_index(P, world, chunks)
+    Pl = gdist.padded_rows(P, world)
+    assert len(set(pos.tolist())) == P
+    assert pos.min() >= 0 and pos.max() < world * Pl
+
+
+def test_shard_range_rejects_bad_args():
+    with pytest.raises(ValueError):
+        gdist.shard_range(10, 0, 0)
+    with pytest.raises(ValueError):
+        gdist.shard_range(10, 2, 2)
