@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--lib", default=None, help="alternative libgna_b200.so (tuning variants)")
     return ap.parse_args()
 
 
@@ -260,7 +261,7 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
-    gna.load()
+    gna.load(args.lib)
     c = workload(args.workload)
     f64 = dict(dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()

@@ -38,15 +38,19 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: dict | None = None) -> str:
+    """Compile csrc/gna_b200.cu; `out`/`defines` build tuning variants (tools/variants.py)."""
+    target = out or LIB
+    if out is None and not force and not stale():
         return LIB
-    tmp = LIB + ".tmp.%d" % os.getpid()
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp,
+    tmp = target + ".tmp.%d" % os.getpid()
+    dflags = ["-D%s=%s" % kv for kv in (defines or {}).items()]
+    cmd = [nvcc(), *NVCC_FLAGS, *dflags, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp,
            os.path.join(CSRC, "gna_b200.cu")]
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

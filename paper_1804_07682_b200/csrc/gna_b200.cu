@@ -13,11 +13,13 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/gna_b200.h"
 #include "gl_table.h"
 #include "gna_device.cuh"
+#include "gna_tma.cuh"
 
 using gna::PeeCoef;
 
@@ -41,7 +43,10 @@ thread_local int t_last_cuda_error = 0;
 
 constexpr int kEvalThreads = 256;
 constexpr int kGLThreads = 64;
-constexpr int kBatchWarps = 4;
+#ifndef GNA_BATCH_WARPS
+#define GNA_BATCH_WARPS 4
+#endif
+constexpr int kBatchWarps = GNA_BATCH_WARPS;
 constexpr int kReduceThreads = 128;
 
 __device__ __forceinline__ int64_t warps_per_point_dev(int64_t nbins) { return (nbins + 31) / 32; }
@@ -89,6 +94,62 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
   } else {
     for (int64_t i = tid; i < n; i += stride) P[i] = gna::pee_inv(c, gna::rcp(E[i]));
   }
+}
+
+// (a3) elementwise P_ee fed by TMA: a persistent block streams 8 KiB tiles of E
+// global -> shared with cp.async.bulk into a kEvalStages-deep ring (mbarrier per
+// stage), so ~kEvalStages x 8 KiB per block stay in flight independently of the
+// registers; threads read their double2 pairs from shared memory, compute, and
+// store P with streaming (evict-first) stores.  Full tiles only; the < 1 tile tail
+// is done by block 0 with plain loads.
+constexpr int kEvalTile = 1024;  // doubles per tile (8 KiB)
+constexpr int kEvalStages = 4;
+constexpr int kEvalTmaThreads = 256;
+
+__global__ void __launch_bounds__(kEvalTmaThreads) k_oscprob_eval_tma(PeeCoef c,
+                                                                       const double* __restrict__ E,
+                                                                       double* __restrict__ P,
+                                                                       int64_t n) {
+  __shared__ alignas(128) double s_buf[kEvalStages][kEvalTile];
+  __shared__ alignas(8) uint64_t s_full[kEvalStages];
+  const int64_t ntiles = n / kEvalTile;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t mine = first < ntiles ? (ntiles - 1 - first) / stride + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kEvalStages; ++st) gna::mbar_init(&s_full[st], 1);
+    gna::fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kEvalStages && st < mine; ++st) {
+      gna::mbar_expect_tx(&s_full[st], kEvalTile * 8);
+      gna::bulk_g2s(s_buf[st], E + (first + st * stride) * kEvalTile, kEvalTile * 8, &s_full[st]);
+    }
+  }
+  for (int64_t it = 0; it < mine; ++it) {
+    const int st = (int)(it % kEvalStages);
+    gna::mbar_wait(&s_full[st], (uint32_t)((it / kEvalStages) & 1));
+    const int64_t tile = first + it * stride;
+    const double2* src = reinterpret_cast<const double2*>(s_buf[st]);
+    double2* dst = reinterpret_cast<double2*>(P + tile * kEvalTile);
+#pragma unroll
+    for (int j = threadIdx.x; j < kEvalTile / 2; j += kEvalTmaThreads) {
+      const double2 e = src[j];
+      double2 r;
+      r.x = gna::pee_inv(c, gna::rcp(e.x));
+      r.y = gna::pee_inv(c, gna::rcp(e.y));
+      __stcs(dst + j, r);
+    }
+    __syncthreads();  // every thread is done with stage st before it is refilled
+    if (threadIdx.x == 0 && it + kEvalStages < mine) {
+      gna::mbar_expect_tx(&s_full[st], kEvalTile * 8);
+      gna::bulk_g2s(s_buf[st], E + (first + (it + kEvalStages) * stride) * kEvalTile,
+                    kEvalTile * 8, &s_full[st]);
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = ntiles * kEvalTile + threadIdx.x; i < n; i += kEvalTmaThreads)
+      P[i] = gna::pee_inv(c, gna::rcp(E[i]));
 }
 
 // (a3)+(a4) one parameter point: one thread per bin, GL nodes from the constant bank.
@@ -198,12 +259,47 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
   }
 }
 
-// (a3)+(a4)+(a5) main pass.  Block = (point p, kBatchWarps x 32 bins); every warp
-// is independent (no block barrier): it copies its point's coefficient row into
-// a warp-private smem slice, then each lane integrates one bin, two GL nodes at a
-// time so each (kq, w) load feeds two sin^2 evaluations.
+#define GNA_PRAGMA(x) _Pragma(#x)
+#define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
+#ifndef GNA_BATCH_NODES
+#define GNA_BATCH_NODES 4
+#endif
+#ifndef GNA_BATCH_JUNROLL
+#define GNA_BATCH_JUNROLL 1
+#endif
+#ifndef GNA_BATCH_MINB
+#define GNA_BATCH_MINB 1
+#endif
+
+// N GL nodes of one bin at a time: each (kq, omega*w) coefficient load from
+// shared memory feeds N independent sin^2 chains (ILP across nodes).
+template <int N>
+__device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int nterm,
+                                            const double* __restrict__ invE,
+                                            const double* __restrict__ hw, int64_t nbins, int i,
+                                            double c0, double& s) {
+  double iE[N], a[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    iE[n] = invE[(int64_t)(i + n) * nbins];
+    a[n] = 0.0;
+  }
+  GNA_UNROLL(GNA_BATCH_JUNROLL)
+  for (int j = 0; j < nterm; ++j) {
+    const double2 cw = sc[j];
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) s = fma(hw[(int64_t)(i + n) * nbins], c0 - a[n], s);
+}
+
+// (a3)+(a4)+(a5) main pass.  Block = (point p, kWarps x 32 bins); every warp is
+// independent (no block barrier): it copies its point's coefficient row into a
+// warp-private smem slice, then each lane integrates one bin, GNA_BATCH_NODES
+// GL nodes at a time.
 template <int kWarps>
-__global__ void __launch_bounds__(kWarps * 32) k_oscprob_batch(
+__global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     int nterm, int order, int64_t nbins, int64_t bpp, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double2 s_coef[];
@@ -225,28 +321,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_oscprob_batch(
   const double* __restrict__ hw = w.hw + kk;
   double s = 0.0;
   int i = 0;
-  for (; i + 1 < order; i += 2) {
-    const double iE0 = invE[(int64_t)i * nbins], iE1 = invE[(int64_t)(i + 1) * nbins];
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < nterm; ++j) {
-      const double2 cw = sc[j];
-      a0 = fma(cw.y, gna::sin2c(cw.x, iE0), a0);
-      a1 = fma(cw.y, gna::sin2c(cw.x, iE1), a1);
-    }
-    s = fma(hw[(int64_t)i * nbins], c0 - a0, s);
-    s = fma(hw[(int64_t)(i + 1) * nbins], c0 - a1, s);
+  for (; i + GNA_BATCH_NODES <= order; i += GNA_BATCH_NODES)
+    batch_nodes<GNA_BATCH_NODES>(sc, nterm, invE, hw, nbins, i, c0, s);
+  if (GNA_BATCH_NODES > 2 && i + 2 <= order) {
+    batch_nodes<2>(sc, nterm, invE, hw, nbins, i, c0, s);
+    i += 2;
   }
-  if (i < order) {
-    const double iE0 = invE[(int64_t)i * nbins];
-    double a0 = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < nterm; ++j) {
-      const double2 cw = sc[j];
-      a0 = fma(cw.y, gna::sin2c(cw.x, iE0), a0);
-    }
-    s = fma(hw[(int64_t)i * nbins], c0 - a0, s);
-  }
+  if (i < order) batch_nodes<1>(sc, nterm, invE, hw, nbins, i, c0, s);
   double x2 = 0.0;
   if (active) {
     if (spectra) spectra[p * nbins + k] = s;
@@ -466,7 +547,12 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
 int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStream_t s) {
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
-  if (vec) {
+  if (vec && n >= (int64_t)kEvalTile * 4) {
+    // persistent TMA-fed stream: 6 blocks per SM (32 KiB smem ring each)
+    const int64_t ntiles = n / kEvalTile;
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 6);
+    k_oscprob_eval_tma<<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
+  } else if (vec) {
     const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);
     k_oscprob_eval<true><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
   } else {

@@ -1,0 +1,42 @@
+"""Build tuning variants of libgna_b200.so (compile-time knobs of the batch kernel) and
+print their register/spill counts.  Measured with bench.py --lib on the GPU box."""
+from __future__ import annotations
+
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1804_07682_b200 import _build  # noqa: E402
+
+VARIANTS = {
+    "n2u4": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4),
+    "n2u2": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2),
+    "n2u1": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=1),
+    "n2u4m16": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4, GNA_BATCH_MINB=16),
+    "n1u4m16": dict(GNA_BATCH_NODES=1, GNA_BATCH_JUNROLL=4, GNA_BATCH_MINB=16),
+    "n4u1": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1),
+    "n4u1m12": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=12),
+    "n2u4w8": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4, GNA_BATCH_WARPS=8),
+    "n2u2w8m6": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2, GNA_BATCH_WARPS=8, GNA_BATCH_MINB=6),
+}
+
+
+def main(names):
+    outdir = os.path.join(ROOT, "build", "variants")
+    os.makedirs(outdir, exist_ok=True)
+    for name in names or VARIANTS:
+        out = os.path.join(outdir, name + ".so")
+        cmd_out = subprocess.run(
+            [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
+             "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
+            capture_output=True, text=True, check=True).stderr
+        m = re.search(r"k_oscprob_batch.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+                      cmd_out, re.S)
+        print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
