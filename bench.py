@@ -39,6 +39,9 @@ UNIT = "energy points/s"
 # minimax 8, weighted accumulate 1).  Per-node work (reciprocal, node position,
 # GL weight) is amortised over baselines and not counted.
 FP64_OPS_PER_EVAL = 39
+# elementwise mode adds the reciprocal of each energy: MUFU.RCP64H (1/3-rate, 3 slots)
+# + 3 DFMA (tools/probe_rcp.cu)
+FP64_OPS_EVAL_MODE = FP64_OPS_PER_EVAL + 6
 FP64_LANES_PER_SM = 64        # measured: tools/probe_fp64.cu, profiles/r01_probe_fp64.jsonl
 SM_COUNT = 148
 
@@ -56,6 +59,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--lib", default=None, help="alternative libgna_b200.so (tuning variants)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay each step as a CUDA graph (auto: when N == 1)")
     return ap.parse_args()
 
 
@@ -83,6 +88,27 @@ def workload(name: str) -> dict:
         c["desc"] = dict(workload="cfg3: 1 parameter point, %d energies streamed from HBM "
                          "(elementwise P_ee)" % c["n"], points=1, energies=c["n"])
     return c
+
+
+class KernelTimer:
+    """CUDA events around one library call on the launching (current) stream."""
+    enabled = True
+
+    def __init__(self, sink):
+        self.sink = sink
+
+    def __enter__(self):
+        if KernelTimer.enabled:
+            import torch
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e1 = torch.cuda.Event(enable_timing=True)
+            self.e0.record()
+        return self
+
+    def __exit__(self, *a):
+        if KernelTimer.enabled:
+            self.e1.record()
+            self.sink.append((self.e0, self.e1))
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -285,19 +311,15 @@ def main():
 
         def compute(vlo, vhi, sp_rows, x2_rows):
             sub = {k: v[vlo:vhi] for k, v in pts.items()}
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            gna.oscprob_batch(sub, L, om, edges, c["order"], data=data, spectra=sp_rows,
-                              chi2=x2_rows, workspace=ws)
-            e1.record()
-            kern_ev.append((e0, e1))
+            with KernelTimer(kern_ev):
+                gna.oscprob_batch(sub, L, om, edges, c["order"], data=data, spectra=sp_rows,
+                                  chi2=x2_rows, workspace=ws)
 
         def step():
             sb.step(compute, comm_stream=comm)
 
         units_per_rank = (hi - lo) * L.size * nb * c["order"]
-        launches_per_step = 2 * len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
+        calls_per_step = len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
         scaling = "strong"
     elif args.workload == "cfg2":
         edges = torch.tensor(c["edges"], **f64)
@@ -305,15 +327,11 @@ def main():
         kern_ev = []
 
         def step():
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            gna.gl_integrate(c["params"], c["L_km"], edges, c["order"], out=out)
-            e1.record()
-            kern_ev.append((e0, e1))
+            with KernelTimer(kern_ev):
+                gna.gl_integrate(c["params"], c["L_km"], edges, c["order"], out=out)
 
         units_per_rank = c["evals"]
-        launches_per_step = 1
+        calls_per_step = 1
         scaling = "weak"  # replicas only
     else:
         E = torch.linspace(c["lo"], c["hi"], c["n"], **f64)
@@ -321,15 +339,11 @@ def main():
         kern_ev = []
 
         def step():
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            gna.oscprob_eval(c["params"], c["L_km"], E, out=out)
-            e1.record()
-            kern_ev.append((e0, e1))
+            with KernelTimer(kern_ev):
+                gna.oscprob_eval(c["params"], c["L_km"], E, out=out)
 
         units_per_rank = c["evals"]
-        launches_per_step = 1
+        calls_per_step = 1
         scaling = "weak"  # replicas only
 
     def barrier():
@@ -342,6 +356,29 @@ def main():
         step()
     torch.cuda.synchronize()
     kern_ev.clear()
+
+    # ---------------- CUDA graph of the step (the repeated-evaluation loop of a fit):
+    # one graph launch per step instead of per-call host work.  NCCL steps stay eager.
+    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1)
+    launches_per_step = None
+    if use_graph:
+        KernelTimer.enabled = False
+        g = torch.cuda.CUDAGraph()
+        n0 = gna.launch_count()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                step()
+        torch.cuda.current_stream().wait_stream(cap)
+        launches_per_step = gna.launch_count() - n0
+        eager_step = step
+
+        def step():  # noqa: F811
+            g.replay()
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
 
     # ---------------- timed region: K steps, per-step events, L2 flushed between steps
     barrier()
@@ -361,7 +398,13 @@ def main():
     barrier()
     launches = gna.launch_count() - n_launch0
     total_ms = sum(a.elapsed_time(b) for a, b in evs)
-    kern_ms = [a.elapsed_time(b) for a, b in kern_ev]
+    if use_graph:
+        # kernels replayed from the graph: count = per-step launches captured x steps;
+        # the step is the dominant kernel plus two us-scale helpers -> step time bounds it
+        launches = launches_per_step * args.steps
+        kern_ms = [a.elapsed_time(b) for a, b in evs]
+    else:
+        kern_ms = [a.elapsed_time(b) for a, b in kern_ev]
     t = torch.tensor([total_ms, float(np.mean(kern_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -381,9 +424,10 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": peaks["source"],
-                "fp64_frac": launch_units * (FP64_OPS_PER_EVAL + 7) / (kern_avg_ms * 1e-3) / peak_ops}
+                "fp64_frac": launch_units * FP64_OPS_PER_EVAL_MODE / (kern_avg_ms * 1e-3) / peak_ops,
+                "fp64_ops_per_energy": FP64_OPS_PER_EVAL_MODE}
     else:
-        launch_units = (units_per_rank / max(launches_per_step // 2, 1)
+        launch_units = (units_per_rank / max(calls_per_step, 1)
                         if args.workload in ("cfg4", "cfg5") else units_per_rank)
         achieved = launch_units * FP64_OPS_PER_EVAL / (kern_avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
@@ -402,7 +446,8 @@ def main():
                            l2="flushed between steps (256 MiB write, untimed)",
                            energy_points_per_step=units_total),
             "bins_per_s": (c["bins_total"] * args.steps / (total_ms * 1e-3)) if c["bins_total"] else None,
-            "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof}
+            "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof,
+            "cuda_graph": bool(use_graph)}
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
     if not args.no_e2e:

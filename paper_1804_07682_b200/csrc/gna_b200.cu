@@ -103,10 +103,10 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
 // store P with streaming (evict-first) stores.  Full tiles only; the < 1 tile tail
 // is done by block 0 with plain loads.
 constexpr int kEvalTile = 1024;  // doubles per tile (8 KiB)
-constexpr int kEvalStages = 4;
+constexpr int kEvalStages = 3;
 constexpr int kEvalTmaThreads = 256;
 
-__global__ void __launch_bounds__(kEvalTmaThreads) k_oscprob_eval_tma(PeeCoef c,
+__global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef c,
                                                                        const double* __restrict__ E,
                                                                        double* __restrict__ P,
                                                                        int64_t n) {
@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kEvalTmaThreads) k_oscprob_eval_tma(PeeCoef c,
       P[i] = gna::pee_inv(c, gna::rcp(E[i]));
 }
 
-// (a3)+(a4) one parameter point: one thread per bin, GL nodes from the constant bank.
+// (a3)+(a4) one parameter point: one thread per bin, GL nodes/weights from the
+// constant bank, two nodes per iteration for two independent reciprocal+sin^2 chains.
 __global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int order,
                                                              const double* __restrict__ edges,
                                                              int64_t nbins,
@@ -164,10 +165,14 @@ __global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int orde
     const double ctr = 0.5 * (e0 + e1);
     const double h = 0.5 * (e1 - e0);
     double s = 0.0;
-    for (int i = 0; i < order; ++i) {
-      const double E = fma(h, c_gl_t[off + i], ctr);
-      s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(E)), s);
+    int i = 0;
+    for (; i + 1 < order; i += 2) {
+      const double p0 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
+      const double p1 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i + 1], ctr)));
+      s = fma(c_gl_w[off + i], p0, s);
+      s = fma(c_gl_w[off + i + 1], p1, s);
     }
+    if (i < order) s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
     bins[k] = h * s;
   }
 }
@@ -548,9 +553,9 @@ int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStr
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
   if (vec && n >= (int64_t)kEvalTile * 4) {
-    // persistent TMA-fed stream: 6 blocks per SM (32 KiB smem ring each)
+    // persistent TMA-fed stream: 8 blocks per SM (24 KiB smem ring each)
     const int64_t ntiles = n / kEvalTile;
-    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 6);
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 8);
     k_oscprob_eval_tma<<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
   } else if (vec) {
     const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);
