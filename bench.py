@@ -424,8 +424,8 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": peaks["source"],
-                "fp64_frac": launch_units * FP64_OPS_PER_EVAL_MODE / (kern_avg_ms * 1e-3) / peak_ops,
-                "fp64_ops_per_energy": FP64_OPS_PER_EVAL_MODE}
+                "fp64_frac": launch_units * FP64_OPS_EVAL_MODE / (kern_avg_ms * 1e-3) / peak_ops,
+                "fp64_ops_per_energy": FP64_OPS_EVAL_MODE}
     else:
         launch_units = (units_per_rank / max(calls_per_step, 1)
                         if args.workload in ("cfg4", "cfg5") else units_per_rank)
