@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <algorithm>
+#include <utility>
 #include <mutex>
 
 #include "../../include/gna_b200.h"
@@ -152,29 +153,50 @@ __global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef
       P[i] = gna::pee_inv(c, gna::rcp(E[i]));
 }
 
-// (a3)+(a4) one parameter point: one thread per bin, GL nodes/weights from the
-// constant bank, two nodes per iteration for two independent reciprocal+sin^2 chains.
+// (a3)+(a4) one parameter point: one thread per bin.  kOrder > 0: the node loop is
+// fully unrolled (orders 1-16), so all nodes are independent reciprocal + sin^2 chains
+// (ILP = order) and the GL nodes/weights are constant-bank operands at fixed offsets;
+// kOrder = 0: runtime order (17-32), two nodes per iteration.
+template <int kOrder>
 __global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int order,
                                                              const double* __restrict__ edges,
                                                              int64_t nbins,
                                                              double* __restrict__ bins) {
-  const int off = GNA_GL_OFF(order);
+  const int n = kOrder > 0 ? kOrder : order;
+  const int off = GNA_GL_OFF(n);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nbins; k += stride) {
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
     const double h = 0.5 * (e1 - e0);
     double s = 0.0;
-    int i = 0;
-    for (; i + 1 < order; i += 2) {
-      const double p0 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
-      const double p1 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i + 1], ctr)));
-      s = fma(c_gl_w[off + i], p0, s);
-      s = fma(c_gl_w[off + i + 1], p1, s);
+    if (kOrder > 0) {
+      double pv[kOrder > 0 ? kOrder : 1];
+#pragma unroll
+      for (int i = 0; i < kOrder; ++i)
+        pv[i] = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
+#pragma unroll
+      for (int i = 0; i < kOrder; ++i) s = fma(c_gl_w[off + i], pv[i], s);
+    } else {
+      int i = 0;
+      for (; i + 1 < n; i += 2) {
+        const double p0 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
+        const double p1 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i + 1], ctr)));
+        s = fma(c_gl_w[off + i], p0, s);
+        s = fma(c_gl_w[off + i + 1], p1, s);
+      }
+      if (i < n) s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
     }
-    if (i < order) s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
     bins[k] = h * s;
   }
+}
+
+using gl_kernel_t = void (*)(PeeCoef, int, const double*, int64_t, double*);
+
+template <int... N>
+constexpr gl_kernel_t gl_kernel_for(int order, std::integer_sequence<int, N...>) {
+  gl_kernel_t t[] = {k_gl_integrate<0>, k_gl_integrate<N + 1>...};
+  return order >= 1 && order <= (int)sizeof...(N) ? t[order] : t[0];
 }
 
 struct BatchSetupArgs {
@@ -642,7 +664,8 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   PeeCoef c;
   make_coef(p, L_km, &c);
   const int grid = grid_for(nbins, kGLThreads, 0x7fffffff);
-  k_gl_integrate<<<grid, kGLThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges, nbins, d_bins);
+  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, 16>{});
+  kern<<<grid, kGLThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges, nbins, d_bins);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);

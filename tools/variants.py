@@ -12,15 +12,15 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "n2u4": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4),
-    "n2u2": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2),
-    "n2u1": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=1),
-    "n2u4m16": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4, GNA_BATCH_MINB=16),
-    "n1u4m16": dict(GNA_BATCH_NODES=1, GNA_BATCH_JUNROLL=4, GNA_BATCH_MINB=16),
     "n4u1": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1),
-    "n4u1m12": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=12),
-    "n2u4w8": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=4, GNA_BATCH_WARPS=8),
-    "n2u2w8m6": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2, GNA_BATCH_WARPS=8, GNA_BATCH_MINB=6),
+    "n4u1m6": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=6),
+    "n4u1m8": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=8),
+    "n3u1": dict(GNA_BATCH_NODES=3, GNA_BATCH_JUNROLL=1),
+    "n3u1m8": dict(GNA_BATCH_NODES=3, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=8),
+    "n4u2m8": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=8),
+    "n5u1": dict(GNA_BATCH_NODES=5, GNA_BATCH_JUNROLL=1),
+    "n5u1m6": dict(GNA_BATCH_NODES=5, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=6),
+    "n2u2m8": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=8),
 }
 
 
