@@ -288,9 +288,6 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 #define GNA_PRAGMA(x) _Pragma(#x)
 #define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
-#ifndef GNA_BATCH_NODES
-#define GNA_BATCH_NODES 4
-#endif
 #ifndef GNA_BATCH_JUNROLL
 #define GNA_BATCH_JUNROLL 1
 #endif
@@ -321,11 +318,26 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
   for (int n = 0; n < N; ++n) s = fma(hw[(int64_t)(i + n) * nbins], c0 - a[n], s);
 }
 
+// remainder of r < N nodes, compile-time group size
+template <int N>
+__device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc, int nterm,
+                                           const double* __restrict__ invE,
+                                           const double* __restrict__ hw, int64_t nbins, int i,
+                                           double c0, double& s) {
+  if constexpr (N > 1) {
+    if (r == N - 1) {
+      batch_nodes<N - 1>(sc, nterm, invE, hw, nbins, i, c0, s);
+      return;
+    }
+    batch_tail<N - 1>(r, sc, nterm, invE, hw, nbins, i, c0, s);
+  }
+}
+
 // (a3)+(a4)+(a5) main pass.  Block = (point p, kWarps x 32 bins); every warp is
 // independent (no block barrier): it copies its point's coefficient row into a
-// warp-private smem slice, then each lane integrates one bin, GNA_BATCH_NODES
-// GL nodes at a time.
-template <int kWarps>
+// warp-private smem slice, then each lane integrates one bin, N GL nodes at a time
+// (N divides the order when possible, so no group runs with reduced ILP).
+template <int kWarps, int N>
 __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     int nterm, int order, int64_t nbins, int64_t bpp, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
@@ -348,13 +360,8 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const double* __restrict__ hw = w.hw + kk;
   double s = 0.0;
   int i = 0;
-  for (; i + GNA_BATCH_NODES <= order; i += GNA_BATCH_NODES)
-    batch_nodes<GNA_BATCH_NODES>(sc, nterm, invE, hw, nbins, i, c0, s);
-  if (GNA_BATCH_NODES > 2 && i + 2 <= order) {
-    batch_nodes<2>(sc, nterm, invE, hw, nbins, i, c0, s);
-    i += 2;
-  }
-  if (i < order) batch_nodes<1>(sc, nterm, invE, hw, nbins, i, c0, s);
+  for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
+  if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
   double x2 = 0.0;
   if (active) {
     if (spectra) spectra[p * nbins + k] = s;
@@ -554,8 +561,13 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
 
   const int nterm = 3 * nbase;
   const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
-  k_oscprob_batch<kBatchWarps><<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
-      nterm, order, nbins, bpp, w, spectra, chi2 ? data : nullptr);
+  // node-group size: 5, 4 or 3 when it divides the order, else 4
+  auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5>
+              : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4>
+              : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3>
+                                 : k_oscprob_batch<kBatchWarps, 4>;
+  kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(nterm, order, nbins, bpp, w, spectra,
+                                                        chi2 ? data : nullptr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);

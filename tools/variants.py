@@ -12,15 +12,13 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "n4u1": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1),
-    "n4u1m6": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=6),
-    "n4u1m8": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=8),
-    "n3u1": dict(GNA_BATCH_NODES=3, GNA_BATCH_JUNROLL=1),
-    "n3u1m8": dict(GNA_BATCH_NODES=3, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=8),
-    "n4u2m8": dict(GNA_BATCH_NODES=4, GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=8),
-    "n5u1": dict(GNA_BATCH_NODES=5, GNA_BATCH_JUNROLL=1),
-    "n5u1m6": dict(GNA_BATCH_NODES=5, GNA_BATCH_JUNROLL=1, GNA_BATCH_MINB=6),
-    "n2u2m8": dict(GNA_BATCH_NODES=2, GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=8),
+    "w4": dict(GNA_BATCH_WARPS=4),
+    "w4m6": dict(GNA_BATCH_WARPS=4, GNA_BATCH_MINB=6),
+    "w2": dict(GNA_BATCH_WARPS=2),
+    "w2m12": dict(GNA_BATCH_WARPS=2, GNA_BATCH_MINB=12),
+    "w1": dict(GNA_BATCH_WARPS=1),
+    "w1m24": dict(GNA_BATCH_WARPS=1, GNA_BATCH_MINB=24),
+    "w8m3": dict(GNA_BATCH_WARPS=8, GNA_BATCH_MINB=3),
 }
 
 
