@@ -45,7 +45,7 @@ thread_local int t_last_cuda_error = 0;
 constexpr int kEvalThreads = 256;
 constexpr int kGLThreads = 64;
 #ifndef GNA_BATCH_WARPS
-#define GNA_BATCH_WARPS 4
+#define GNA_BATCH_WARPS 1
 #endif
 constexpr int kBatchWarps = GNA_BATCH_WARPS;
 constexpr int kReduceThreads = 128;
@@ -339,42 +339,45 @@ __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc
 // (N divides the order when possible, so no group runs with reduced ILP).
 template <int kWarps, int N>
 __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
-    int nterm, int order, int64_t nbins, int64_t bpp, BatchWs w,
+    int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double2 s_coef[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = blockIdx.x / bpp;
-  const int64_t wt = (blockIdx.x - p * bpp) * kWarps + warp;  // warp tile within the point
+  const int64_t pg = blockIdx.x / bpp;                          // point group
+  const int64_t wt = (blockIdx.x - pg * bpp) * kWarps + warp;  // warp tile within a point
   const int64_t k0 = wt * 32;
   if (k0 >= nbins) return;  // whole warp
   double2* sc = s_coef + warp * nterm;
-  const double2* __restrict__ gc = w.coef + p * nterm;
-  for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
-  __syncwarp();
-
   const int64_t k = k0 + lane;
   const bool active = k < nbins;
   const int64_t kk = active ? k : nbins - 1;
-  const double c0 = w.c0[p];
   const double* __restrict__ invE = w.invE + kk;
   const double* __restrict__ hw = w.hw + kk;
-  double s = 0.0;
-  int i = 0;
-  for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
-  if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
-  double x2 = 0.0;
-  if (active) {
-    if (spectra) spectra[p * nbins + k] = s;
-    if (data) {
-      const double D = data[k];
+  const double D = (data && active) ? data[k] : 1.0;
+  const int64_t wpp = warps_per_point_dev(nbins);
+  // ppw points per warp, same bins: the node tables stay in L1 across points
+  const int64_t pend = min(npoints, (pg + 1) * (int64_t)ppw);
+  for (int64_t p = pg * (int64_t)ppw; p < pend; ++p) {
+    const double2* __restrict__ gc = w.coef + p * nterm;
+    __syncwarp();  // previous point's reads of sc are done
+    for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
+    __syncwarp();
+    const double c0 = w.c0[p];
+    double s = 0.0;
+    int i = 0;
+    for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
+    if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
+    double x2 = 0.0;
+    if (active) {
+      if (spectra) spectra[p * nbins + k] = s;
       const double d = s - D;
       x2 = d * d / D;
     }
-  }
-  if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
+    if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-    if (lane == 0) w.partial[p * warps_per_point_dev(nbins) + wt] = x2;
+      for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
+    }
   }
 }
 
@@ -549,7 +552,14 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
   a.npoints = pts->npoints;
   const BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
   const int64_t bpp = blocks_per_point(nbins);
-  const int64_t nblocks = pts->npoints * bpp;
+  // points per warp: enough sin^2 work per lane (>= ~240) to amortise the per-point
+  // overhead, while keeping >= 16 warps per SM worth of blocks
+  const int64_t work = (int64_t)3 * nbase * order;
+  int64_t ppw = std::max<int64_t>(1, (240 + work - 1) / work);
+  const int64_t min_blocks = (int64_t)sm_count() * 16;
+  while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
+  const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;
+  const int64_t nblocks = ngroups * bpp;
   const int64_t nsetup = pts->npoints * nbase + (int64_t)order * nbins;
   if (nblocks > 0x7fffffffLL || (nsetup + 255) / 256 > 0x7fffffffLL) return GNA_EINVAL;
 
@@ -566,8 +576,8 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4>
               : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3>
                                  : k_oscprob_batch<kBatchWarps, 4>;
-  kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(nterm, order, nbins, bpp, w, spectra,
-                                                        chi2 ? data : nullptr);
+  kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
+      nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
