@@ -355,18 +355,14 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const double* __restrict__ hw = w.hw + kk;
   const double D = (data && active) ? data[k] : 1.0;
   const int64_t wpp = warps_per_point_dev(nbins);
-  // ppw points per warp, same bins: the node tables stay in L1 across points.  The
-  // next point's coefficient row and c0 are loaded into registers while the current
-  // point computes (software pipelining hides the L2 latency of the per-point loads).
-  const int64_t p0 = pg * (int64_t)ppw;
-  const int64_t pend = min(npoints, p0 + (int64_t)ppw);
-  for (int j = lane; j < nterm; j += 32) sc[j] = w.coef[p0 * nterm + j];
-  double c0 = w.c0[p0];
-  __syncwarp();
-  for (int64_t p = p0; p < pend; ++p) {
-    const bool more = p + 1 < pend;
-    const double2 nxt = (more && lane < nterm) ? w.coef[(p + 1) * nterm + lane] : make_double2(0, 0);
-    const double c0n = more ? w.c0[p + 1] : 0.0;
+  // ppw points per warp, same bins: the node tables stay in L1 across points
+  const int64_t pend = min(npoints, (pg + 1) * (int64_t)ppw);
+  for (int64_t p = pg * (int64_t)ppw; p < pend; ++p) {
+    const double2* __restrict__ gc = w.coef + p * nterm;
+    __syncwarp();  // previous point's reads of sc are done
+    for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
+    __syncwarp();
+    const double c0 = w.c0[p];
     double s = 0.0;
     int i = 0;
     for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
@@ -381,13 +377,6 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
       if (lane == 0) w.partial[p * wpp + wt] = x2;
-    }
-    if (more) {
-      __syncwarp();  // every lane is done reading sc for point p
-      if (lane < nterm) sc[lane] = nxt;
-      for (int j = lane + 32; j < nterm; j += 32) sc[j] = w.coef[(p + 1) * nterm + j];
-      c0 = c0n;
-      __syncwarp();
     }
   }
 }
