@@ -43,7 +43,6 @@ std::atomic<int64_t> g_launches{0};
 thread_local int t_last_cuda_error = 0;
 
 constexpr int kEvalThreads = 256;
-constexpr int kGLThreads = 64;
 #ifndef GNA_BATCH_WARPS
 #define GNA_BATCH_WARPS 1
 #endif
@@ -153,50 +152,40 @@ __global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef
       P[i] = gna::pee_inv(c, gna::rcp(E[i]));
 }
 
-// (a3)+(a4) one parameter point: one thread per bin.  kOrder > 0: the node loop is
-// fully unrolled (orders 1-16), so all nodes are independent reciprocal + sin^2 chains
-// (ILP = order) and the GL nodes/weights are constant-bank operands at fixed offsets;
-// kOrder = 0: runtime order (17-32), two nodes per iteration.
-template <int kOrder>
-__global__ void __launch_bounds__(kGLThreads) k_gl_integrate(PeeCoef c, int order,
-                                                             const double* __restrict__ edges,
-                                                             int64_t nbins,
-                                                             double* __restrict__ bins) {
-  const int n = kOrder > 0 ? kOrder : order;
-  const int off = GNA_GL_OFF(n);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nbins; k += stride) {
+// (a3)+(a4) one parameter point.  Thread = (bin, GL node): a warp covers
+// floor(32/order) bins, lane l evaluating node l % order of bin l / order, so 10^5
+// bins x 10 nodes run as 10^6 independent reciprocal + 3 sin^2 chains (enough warps
+// to hide the FP64 latency on 148 SMs); the node sums go through shared memory and
+// are added by the bin's node-0 lane in node order.  GL nodes/weights come from the
+// constant bank.
+constexpr int kGLLaneThreads = 256;
+
+__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c, int order,
+                                                                 const double* __restrict__ edges,
+                                                                 int64_t nbins,
+                                                                 double* __restrict__ bins) {
+  __shared__ double s_v[kGLLaneThreads];
+  const int lane = threadIdx.x & 31;
+  const int bpw = 32 / order;  // bins per warp
+  const int64_t gw = (int64_t)blockIdx.x * (kGLLaneThreads / 32) + (threadIdx.x >> 5);
+  const int b_in = lane / order, node = lane - b_in * order;
+  const int64_t k = gw * bpw + b_in;
+  const bool act = b_in < bpw && k < nbins;
+  const int off = GNA_GL_OFF(order);
+  double v = 0.0, h = 0.0;
+  if (act) {
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
-    const double h = 0.5 * (e1 - e0);
+    h = 0.5 * (e1 - e0);
+    v = c_gl_w[off + node] * gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + node], ctr)));
+  }
+  s_v[threadIdx.x] = v;
+  __syncwarp();
+  if (act && node == 0) {
     double s = 0.0;
-    if (kOrder > 0) {
-      double pv[kOrder > 0 ? kOrder : 1];
-#pragma unroll
-      for (int i = 0; i < kOrder; ++i)
-        pv[i] = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
-#pragma unroll
-      for (int i = 0; i < kOrder; ++i) s = fma(c_gl_w[off + i], pv[i], s);
-    } else {
-      int i = 0;
-      for (; i + 1 < n; i += 2) {
-        const double p0 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr)));
-        const double p1 = gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i + 1], ctr)));
-        s = fma(c_gl_w[off + i], p0, s);
-        s = fma(c_gl_w[off + i + 1], p1, s);
-      }
-      if (i < n) s = fma(c_gl_w[off + i], gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
-    }
+    for (int i = 0; i < order; ++i) s += s_v[threadIdx.x + i];
     bins[k] = h * s;
   }
-}
-
-using gl_kernel_t = void (*)(PeeCoef, int, const double*, int64_t, double*);
-
-template <int... N>
-constexpr gl_kernel_t gl_kernel_for(int order, std::integer_sequence<int, N...>) {
-  gl_kernel_t t[] = {k_gl_integrate<0>, k_gl_integrate<N + 1>...};
-  return order >= 1 && order <= (int)sizeof...(N) ? t[order] : t[0];
 }
 
 struct BatchSetupArgs {
@@ -685,9 +674,12 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  const int grid = grid_for(nbins, kGLThreads, 0x7fffffff);
-  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, 16>{});
-  kern<<<grid, kGLThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges, nbins, d_bins);
+  const int64_t bpw = 32 / order;
+  const int64_t warps = (nbins + bpw - 1) / bpw;
+  const int64_t grid = (warps + kGLLaneThreads / 32 - 1) / (kGLLaneThreads / 32);
+  if (grid > 0x7fffffffLL) return GNA_EINVAL;
+  k_gl_integrate<<<(unsigned)grid, kGLLaneThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges,
+                                                                              nbins, d_bins);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
