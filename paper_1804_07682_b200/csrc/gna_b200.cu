@@ -36,6 +36,10 @@ constexpr double kMeV2Over_pi = 636.6197723675813430755;  // 2000/pi
 
 __constant__ double c_gl_t[GNA_GL_TABLE_SIZE] = GNA_GL_NODES_INIT;
 __constant__ double c_gl_w[GNA_GL_TABLE_SIZE] = GNA_GL_WEIGHTS_INIT;
+// global-memory copy for lane-divergent indexing (the constant cache serialises
+// a warp's distinct addresses; L1 serves them in one wavefront)
+__device__ double g_gl_t[GNA_GL_TABLE_SIZE] = GNA_GL_NODES_INIT;
+__device__ double g_gl_w[GNA_GL_TABLE_SIZE] = GNA_GL_WEIGHTS_INIT;
 const double h_gl_t[GNA_GL_TABLE_SIZE] = GNA_GL_NODES_INIT;
 const double h_gl_w[GNA_GL_TABLE_SIZE] = GNA_GL_WEIGHTS_INIT;
 
@@ -156,8 +160,8 @@ __global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef
 // floor(32/order) bins, lane l evaluating node l % order of bin l / order, so 10^5
 // bins x 10 nodes run as 10^6 independent reciprocal + 3 sin^2 chains (enough warps
 // to hide the FP64 latency on 148 SMs); the node sums go through shared memory and
-// are added by the bin's node-0 lane in node order.  GL nodes/weights come from the
-// constant bank.
+// are added by the bin's node-0 lane in node order.  GL nodes/weights are read
+// per lane from a global copy of the table (L1).
 constexpr int kGLLaneThreads = 256;
 
 __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c, int order,
@@ -177,7 +181,8 @@ __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c, int 
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
     h = 0.5 * (e1 - e0);
-    v = c_gl_w[off + node] * gna::pee_inv(c, gna::rcp(fma(h, c_gl_t[off + node], ctr)));
+    v = __ldg(&g_gl_w[off + node]) *
+        gna::pee_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
   }
   s_v[threadIdx.x] = v;
   __syncwarp();
