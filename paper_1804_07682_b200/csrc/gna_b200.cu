@@ -164,18 +164,19 @@ __global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef
 // per lane from a global copy of the table (L1).
 constexpr int kGLLaneThreads = 256;
 
-__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c, int order,
+template <int kOrder>
+__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c,
                                                                  const double* __restrict__ edges,
                                                                  int64_t nbins,
                                                                  double* __restrict__ bins) {
+  constexpr int bpw = 32 / kOrder;  // bins per warp
+  constexpr int off = GNA_GL_OFF(kOrder);
   __shared__ double s_v[kGLLaneThreads];
   const int lane = threadIdx.x & 31;
-  const int bpw = 32 / order;  // bins per warp
   const int64_t gw = (int64_t)blockIdx.x * (kGLLaneThreads / 32) + (threadIdx.x >> 5);
-  const int b_in = lane / order, node = lane - b_in * order;
+  const int b_in = lane / kOrder, node = lane - b_in * kOrder;
   const int64_t k = gw * bpw + b_in;
   const bool act = b_in < bpw && k < nbins;
-  const int off = GNA_GL_OFF(order);
   double v = 0.0, h = 0.0;
   if (act) {
     const double e0 = edges[k], e1 = edges[k + 1];
@@ -188,9 +189,18 @@ __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c, int 
   __syncwarp();
   if (act && node == 0) {
     double s = 0.0;
-    for (int i = 0; i < order; ++i) s += s_v[threadIdx.x + i];
+#pragma unroll
+    for (int i = 0; i < kOrder; ++i) s += s_v[threadIdx.x + i];
     bins[k] = h * s;
   }
+}
+
+using gl_kernel_t = void (*)(PeeCoef, const double*, int64_t, double*);
+
+template <int... N>
+gl_kernel_t gl_kernel_for(int order, std::integer_sequence<int, N...>) {
+  static const gl_kernel_t t[] = {k_gl_integrate<N + 1>...};
+  return t[order - 1];
 }
 
 struct BatchSetupArgs {
@@ -683,8 +693,8 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   const int64_t warps = (nbins + bpw - 1) / bpw;
   const int64_t grid = (warps + kGLLaneThreads / 32 - 1) / (kGLLaneThreads / 32);
   if (grid > 0x7fffffffLL) return GNA_EINVAL;
-  k_gl_integrate<<<(unsigned)grid, kGLLaneThreads, 0, (cudaStream_t)stream>>>(c, order, d_edges,
-                                                                              nbins, d_bins);
+  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+  kern<<<(unsigned)grid, kGLLaneThreads, 0, (cudaStream_t)stream>>>(c, d_edges, nbins, d_bins);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
