@@ -156,43 +156,43 @@ __global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef
       P[i] = gna::pee_inv(c, gna::rcp(E[i]));
 }
 
-// (a3)+(a4) one parameter point.  Thread = (bin, GL node): a warp covers
-// floor(32/order) bins, lane l evaluating node l % order of bin l / order, so 10^5
-// bins x 10 nodes run as 10^6 independent reciprocal + 3 sin^2 chains (enough warps
-// to hide the FP64 latency on 148 SMs); the node sums go through shared memory and
-// are added by the bin's node-0 lane in node order.  GL nodes/weights are read
-// per lane from a global copy of the table (L1).
-constexpr int kGLLaneThreads = 256;
+// (a3)+(a4) one parameter point.  A lane pair owns one bin: lane 2m+h evaluates the
+// nodes [h*H, min((h+1)*H, order)), H = ceil(order/2), fully unrolled (compile-time
+// order), so each lane runs H independent reciprocal + 3 sin^2 chains; the two
+// halves are combined with one shuffle.  The whole grid is resident in one wave, so
+// the bin edges' DRAM latency is paid once.  GL nodes/weights are read per lane
+// from a global (L1) copy of the table.
+constexpr int kGLLaneThreads = 128;
 
 template <int kOrder>
 __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c,
                                                                  const double* __restrict__ edges,
                                                                  int64_t nbins,
                                                                  double* __restrict__ bins) {
-  constexpr int bpw = 32 / kOrder;  // bins per warp
+  constexpr int H = (kOrder + 1) / 2;
   constexpr int off = GNA_GL_OFF(kOrder);
-  __shared__ double s_v[kGLLaneThreads];
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * (kGLLaneThreads / 32) + (threadIdx.x >> 5);
-  const int b_in = lane / kOrder, node = lane - b_in * kOrder;
-  const int64_t k = gw * bpw + b_in;
-  const bool act = b_in < bpw && k < nbins;
-  double v = 0.0, h = 0.0;
-  if (act) {
-    const double e0 = edges[k], e1 = edges[k + 1];
-    const double ctr = 0.5 * (e0 + e1);
-    h = 0.5 * (e1 - e0);
-    v = __ldg(&g_gl_w[off + node]) *
-        gna::pee_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
-  }
-  s_v[threadIdx.x] = v;
-  __syncwarp();
-  if (act && node == 0) {
-    double s = 0.0;
+  const int64_t t = (int64_t)blockIdx.x * kGLLaneThreads + threadIdx.x;
+  const int64_t k = t >> 1;
+  const int half = (int)(t & 1);
+  const bool act = k < nbins;
+  const int64_t kk = act ? k : nbins - 1;
+  const double e0 = edges[kk], e1 = edges[kk + 1];
+  const double ctr = 0.5 * (e0 + e1);
+  const double h = 0.5 * (e1 - e0);
+  double pv[H];
 #pragma unroll
-    for (int i = 0; i < kOrder; ++i) s += s_v[threadIdx.x + i];
-    bins[k] = h * s;
+  for (int i = 0; i < H; ++i) {
+    const int node = half * H + i;
+    pv[i] = 0.0;
+    if (node < kOrder)
+      pv[i] = __ldg(&g_gl_w[off + node]) *
+              gna::pee_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
   }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) s += pv[i];
+  const double other = __shfl_xor_sync(0xffffffffu, s, 1);
+  if (act && half == 0) bins[k] = h * (s + other);
 }
 
 using gl_kernel_t = void (*)(PeeCoef, const double*, int64_t, double*);
@@ -689,9 +689,7 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  const int64_t bpw = 32 / order;
-  const int64_t warps = (nbins + bpw - 1) / bpw;
-  const int64_t grid = (warps + kGLLaneThreads / 32 - 1) / (kGLLaneThreads / 32);
+  const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
   if (grid > 0x7fffffffLL) return GNA_EINVAL;
   const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
   kern<<<(unsigned)grid, kGLLaneThreads, 0, (cudaStream_t)stream>>>(c, d_edges, nbins, d_bins);
