@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg2", "cfg3"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "cfg2", "cfg1"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunks", type=int, default=0, help="gather pipeline chunks (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -76,6 +76,13 @@ def workload(name: str) -> dict:
                          "(%d bins x GL%d), spectra + chi2 per point" % (
                              name, c["L_km"].size, P, nb * c["order"], nb, c["order"]),
                          points=P, baselines=int(c["L_km"].size), bins=nb, order=c["order"])
+    elif name == "cfg1":
+        nb = c["edges"].size - 1
+        c["evals"] = c["E"].size + nb * c["order"]
+        c["bins_total"] = nb
+        c["desc"] = dict(workload="cfg1: 1 parameter point, %d energies (eval) + %d bins x GL%d "
+                         "(DESIGN.md R11)" % (c["E"].size, nb, c["order"]), points=1, bins=nb,
+                         order=c["order"])
     elif name == "cfg2":
         nb = c["edges"].size - 1
         c["evals"] = nb * c["order"]
@@ -190,6 +197,10 @@ def run_reference(args, rank, world):
             e = c["edges"][:ns + 1]
             oracle.gl_integrate(c["params"], c["L_km"], e, c["order"], nthreads=nt)
             u = ns * c["order"]
+        elif args.workload == "cfg1":
+            oracle.prob_array(c["params"], c["L_km"], c["E"], nthreads=nt)
+            oracle.gl_integrate(c["params"], c["L_km"], c["edges"], c["order"], nthreads=nt)
+            u = c["evals"]
         else:
             E = np.linspace(c["lo"], c["hi"], ns)
             oracle.prob_array(c["params"], c["L_km"], E, nthreads=nt)
@@ -201,7 +212,8 @@ def run_reference(args, rank, world):
     dt, u = one_step()
     rate = u / max(dt, 1e-9)
     per_step = max(0.05, min(args.cpu_seconds, 120.0) / max(args.steps + args.warmup, 1))
-    full = {"cfg4": 10_000, "cfg5": 1000, "cfg2": 100_000, "cfg3": 100_000_000}[args.workload]
+    full = {"cfg4": 10_000, "cfg5": 1000, "cfg2": 100_000, "cfg3": 100_000_000,
+            "cfg1": 100}[args.workload]
     unit_per = u / ns
     ns = int(max(1, min(full, rate * per_step / unit_per)))
     for _ in range(args.warmup):
@@ -252,6 +264,16 @@ def cpu_baseline(c, name, seconds):
         dt = time.perf_counter() - t0
         units = (c["edges"].size - 1) * c["order"]
         sample = "full cfg2"
+    elif name == "cfg1":
+        reps = 200
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.prob_array(c["params"], c["L_km"], c["E"], nthreads=1)
+            oracle.gl_integrate(c["params"], c["L_km"], c["edges"], c["order"], nthreads=1)
+        dt = time.perf_counter() - t0
+        units = c["evals"] * reps
+        nt = 1
+        sample = "full cfg1 x %d repetitions, 1 thread" % reps
     else:
         n = 20_000_000
         E = np.linspace(c["lo"], c["hi"], n)
@@ -321,6 +343,21 @@ def main():
         units_per_rank = (hi - lo) * L.size * nb * c["order"]
         calls_per_step = len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
         scaling = "strong"
+    elif args.workload == "cfg1":
+        edges = torch.tensor(c["edges"], **f64)
+        out = torch.empty(c["edges"].size - 1, **f64)
+        E1 = torch.tensor(c["E"], **f64)
+        P1 = torch.empty_like(E1)
+        kern_ev = []
+
+        def step():
+            with KernelTimer(kern_ev):
+                gna.oscprob_eval(c["params"], c["L_km"], E1, out=P1)
+                gna.gl_integrate(c["params"], c["L_km"], edges, c["order"], out=out)
+
+        units_per_rank = c["evals"]
+        calls_per_step = 1
+        scaling = "weak"  # replicas only
     elif args.workload == "cfg2":
         edges = torch.tensor(c["edges"], **f64)
         out = torch.empty(c["edges"].size - 1, **f64)
@@ -511,20 +548,24 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
         h2d = 4 * (hi - lo) * 8 + edges.nbytes + data.nbytes
         d2h = spectra.nbytes + chi2.nbytes
         units = (hi - lo) * c["L_km"].size * nb * c["order"]
-    elif args.workload == "cfg2":
+    elif args.workload in ("cfg1", "cfg2"):
         te, edges = pinned(c["edges"])
         ts, out = pinned(np.empty(c["edges"].size - 1))
         keep = [te, ts]
-        E_host = None
+        if args.workload == "cfg1":
+            tE, E1 = pinned(c["E"])
+            tP, P1 = pinned(np.empty(c["E"].size))
+            keep += [tE, tP]
 
         def one():
-            # host variant of gl_integrate = H2D edges, kernel, D2H bins
-            d_edges = torch.from_numpy(edges).to(dev, non_blocking=True)
-            b = gna.gl_integrate(c["params"], c["L_km"], d_edges, c["order"])
-            ts.copy_(b, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+            if args.workload == "cfg1":
+                gna.oscprob_eval_host(c["params"], c["L_km"], E1, out=P1)
+            gna.gl_integrate_host(c["params"], c["L_km"], edges, c["order"], out=out)
 
         h2d, d2h = edges.nbytes, out.nbytes
+        if args.workload == "cfg1":
+            h2d += E1.nbytes
+            d2h += P1.nbytes
         units = c["evals"]
     else:
         n = c["n"]
@@ -551,13 +592,14 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    total_units = units * world if args.workload in ("cfg2", "cfg3") else c["evals"]
+    total_units = units * world if args.workload in ("cfg1", "cfg2", "cfg3") else c["evals"]
     del keep
     return {"value": total_units * steps / (float(ms[0]) * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": steps, "api": "gna_oscprob_batch_host" if args.workload in ("cfg4", "cfg5")
-            else ("gna_gl_integrate + torch copies" if args.workload == "cfg2"
-                  else "gna_oscprob_eval_host")}
+            else ("gna_gl_integrate_host" if args.workload == "cfg2" else
+                  ("gna_oscprob_eval_host + gna_gl_integrate_host" if args.workload == "cfg1"
+                   else "gna_oscprob_eval_host"))}
 
 
 if __name__ == "__main__":

@@ -155,6 +155,10 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
                           double* h_P, int64_t chunk, void* stream);
 
+int gna_gl_integrate_host(const gna_osc_params* p, double L_km, const double* h_edges,
+                          int64_t nbins, int32_t order, double* h_bins, int64_t chunk,
+                          void* stream);
+
 int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, const double* omega,
                            int32_t nbase, const double* h_edges, int64_t nbins, int32_t order,
                            double* h_spectra, const double* h_data, double* h_chi2,

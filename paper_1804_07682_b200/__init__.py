@@ -22,7 +22,8 @@ from . import _build
 
 __all__ = [
     "GnaError", "OscParams", "load", "oscprob_eval", "gl_integrate", "oscprob_batch",
-    "oscprob_batch_workspace_size", "oscprob_eval_host", "oscprob_batch_host", "gl_rule",
+    "oscprob_batch_workspace_size", "oscprob_eval_host", "gl_integrate_host",
+    "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
 ]
 
@@ -33,7 +34,8 @@ GNA_MAX_NBASE = 64
 # every symbol include/gna_b200.h declares
 EXPORTS = (
     "gna_oscprob_eval", "gna_gl_integrate", "gna_oscprob_batch_workspace_size",
-    "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_oscprob_batch_host", "gna_release",
+    "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_gl_integrate_host",
+    "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
 )
 
@@ -108,6 +110,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_oscprob_batch.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
     L.gna_oscprob_eval_host.argtypes = [P, d, vp, i64, vp, i64, vp]
     L.gna_oscprob_batch_host.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, i64, vp]
+    L.gna_gl_integrate_host.argtypes = [P, d, vp, i64, i32, vp, i64, vp]
     L.gna_release.argtypes = []
     L.gna_release.restype = None
     L.gna_gl_rule.argtypes = [i32, vp, vp]
@@ -118,7 +121,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_launch_count.argtypes = []
     L.gna_launch_count.restype = i64
     for name in ("gna_oscprob_eval", "gna_gl_integrate", "gna_oscprob_batch",
-                 "gna_oscprob_eval_host", "gna_oscprob_batch_host", "gna_gl_rule",
+                 "gna_oscprob_eval_host", "gna_gl_integrate_host", "gna_oscprob_batch_host",
+                 "gna_gl_rule",
                  "gna_last_cuda_error", "gna_abi_version"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
@@ -246,6 +250,22 @@ def oscprob_eval_host(params, L_km: float, E: np.ndarray, out: np.ndarray | None
     _check(L.gna_oscprob_eval_host(ctypes.byref(p), float(L_km), E.ctypes.data, E.size,
                                    out.ctypes.data, int(chunk), _stream(stream)),
            "gna_oscprob_eval_host")
+    return out
+
+
+def gl_integrate_host(params, L_km: float, edges: np.ndarray, order: int,
+                      out: np.ndarray | None = None, chunk: int = 0, stream=None) -> np.ndarray:
+    """Per-bin GL integrals over HOST bin edges (chunked H2D / kernel / D2H)."""
+    L = load()
+    edges = _host(edges, "edges")
+    nbins = edges.size - 1
+    if out is None:
+        out = np.empty(max(nbins, 0))
+    _host(out, "out", max(nbins, 0), writable=True)
+    p = OscParams.of(params)._c()
+    _check(L.gna_gl_integrate_host(ctypes.byref(p), float(L_km), edges.ctypes.data, nbins,
+                                   int(order), out.ctypes.data, int(chunk), _stream(stream)),
+           "gna_gl_integrate_host")
     return out
 
 

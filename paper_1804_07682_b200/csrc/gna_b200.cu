@@ -597,6 +597,17 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
   return GNA_OK;
 }
 
+int launch_gl(const PeeCoef& c, const double* edges, int64_t nbins, int order, double* bins,
+              cudaStream_t s) {
+  const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
+  if (grid > 0x7fffffffLL) return GNA_EINVAL;
+  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+  kern<<<(unsigned)grid, kGLLaneThreads, 0, s>>>(c, edges, nbins, bins);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+
 int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStream_t s) {
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
@@ -689,13 +700,48 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
-  if (grid > 0x7fffffffLL) return GNA_EINVAL;
-  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
-  kern<<<(unsigned)grid, kGLLaneThreads, 0, (cudaStream_t)stream>>>(c, d_edges, nbins, d_bins);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+  return launch_gl(c, d_edges, nbins, order, d_bins, (cudaStream_t)stream);
+}
+
+int gna_gl_integrate_host(const gna_osc_params* p, double L_km, const double* h_edges,
+                          int64_t nbins, int32_t order, double* h_bins, int64_t chunk,
+                          void* stream) {
+  int rc = validate_gl(p, L_km, h_edges, nbins, order, h_bins);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Staging* S = &g_stage[dev];
+  if ((rc = stage_init(S))) return rc;
+  if (chunk <= 0) chunk = (int64_t)1 << 20;  // bins per chunk
+  if (chunk > nbins) chunk = nbins;
+  const size_t need = (size_t)(2 * chunk + 2) * 8;  // edges (chunk+1) + bins (chunk), aligned
+  for (int i = 0; i < 2; ++i)
+    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  PeeCoef c;
+  make_coef(p, L_km, &c);
+  cudaError_t e = cudaEventRecord(S->ev_in, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e);
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+  const int64_t nchunks = (nbins + chunk - 1) / chunk;
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int si = (int)(ci & 1);
+    cudaStream_t s = S->st[si];
+    const int64_t o = ci * chunk;
+    const int64_t m = (o + chunk <= nbins) ? chunk : nbins - o;
+    double* dEd = (double*)S->buf[si];
+    double* dB = dEd + chunk + 2;
+    if ((e = cudaMemcpyAsync(dEd, h_edges + o, (size_t)(m + 1) * 8, cudaMemcpyHostToDevice, s)))
+      return cuda_fail(e);
+    if ((rc = launch_gl(c, dEd, m, order, dB, s))) return rc;
+    if ((e = cudaMemcpyAsync(h_bins + o, dB, (size_t)m * 8, cudaMemcpyDeviceToHost, s)))
+      return cuda_fail(e);
+  }
+  for (int i = 0; i < 2; ++i)
+    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
+  return GNA_OK;
 }
 
 size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t nbins,

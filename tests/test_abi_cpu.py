@@ -102,6 +102,10 @@ def test_gl_einval(lib, case):
                              case.get("nbins", 10), case.get("order", 5), case.get("bins", BAD2),
                              None)
     assert r == gna.GNA_EINVAL
+    r = lib.gna_gl_integrate_host(_params(), case.get("L", 52.5), case.get("edges", BAD),
+                                  case.get("nbins", 10), case.get("order", 5),
+                                  case.get("bins", BAD2), 0, None)
+    assert r == gna.GNA_EINVAL
 
 
 def _batch(lib, host=False, **kw):

@@ -265,6 +265,16 @@ def test_eval_host_bitwise_equals_device(gna):
     assert np.array_equal(Ph, Pd)
 
 
+def test_gl_integrate_host_bitwise_equals_device(gna):
+    g = synth.rng(53)
+    p = synth.random_params(g)
+    edges = np.sort(g.uniform(1.0, 10.0, 100_001))
+    for order in (5, 10, 17):
+        bh = gna.gl_integrate_host(p, 60.0, edges, order, chunk=7_777)
+        bd = _np(gna.gl_integrate(p, 60.0, _t(edges), order))
+        assert np.array_equal(bh, bd)
+
+
 def test_batch_host_bitwise_equals_device(gna):
     g = synth.rng(52)
     pts, L, om, edges, data = _batch_case(g, 11, 3, 257, 6)
