@@ -106,11 +106,23 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
 // registers; threads read their double2 pairs from shared memory, compute, and
 // store P with streaming (evict-first) stores.  Full tiles only; the < 1 tile tail
 // is done by block 0 with plain loads.
-constexpr int kEvalTile = 1024;  // doubles per tile (8 KiB)
-constexpr int kEvalStages = 3;
-constexpr int kEvalTmaThreads = 256;
+#ifndef GNA_EVAL_TILE
+#define GNA_EVAL_TILE 1024
+#endif
+#ifndef GNA_EVAL_STAGES
+#define GNA_EVAL_STAGES 3
+#endif
+#ifndef GNA_EVAL_MINB
+#define GNA_EVAL_MINB 8
+#endif
+#ifndef GNA_EVAL_THREADS
+#define GNA_EVAL_THREADS 256
+#endif
+constexpr int kEvalTile = GNA_EVAL_TILE;  // doubles per tile (8 KiB)
+constexpr int kEvalStages = GNA_EVAL_STAGES;
+constexpr int kEvalTmaThreads = GNA_EVAL_THREADS;
 
-__global__ void __launch_bounds__(kEvalTmaThreads, 8) k_oscprob_eval_tma(PeeCoef c,
+__global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval_tma(PeeCoef c,
                                                                        const double* __restrict__ E,
                                                                        double* __restrict__ P,
                                                                        int64_t n) {
@@ -612,9 +624,9 @@ int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStr
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
   if (vec && n >= (int64_t)kEvalTile * 4) {
-    // persistent TMA-fed stream: 8 blocks per SM (24 KiB smem ring each)
+    // persistent TMA-fed stream: GNA_EVAL_MINB blocks per SM (3 x 8 KiB smem ring each)
     const int64_t ntiles = n / kEvalTile;
-    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 8);
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * GNA_EVAL_MINB);
     k_oscprob_eval_tma<<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
   } else if (vec) {
     const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);

@@ -12,13 +12,12 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "w4": dict(GNA_BATCH_WARPS=4),
-    "w4m6": dict(GNA_BATCH_WARPS=4, GNA_BATCH_MINB=6),
-    "w2": dict(GNA_BATCH_WARPS=2),
-    "w2m12": dict(GNA_BATCH_WARPS=2, GNA_BATCH_MINB=12),
-    "w1": dict(GNA_BATCH_WARPS=1),
-    "w1m24": dict(GNA_BATCH_WARPS=1, GNA_BATCH_MINB=24),
-    "w8m3": dict(GNA_BATCH_WARPS=8, GNA_BATCH_MINB=3),
+    "e_t1k_s3_m8": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=8),
+    "e_t1k_s4_m6": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=6),
+    "e_t1k_s3_m6": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=6),
+    "e_t2k_s2_m6": dict(GNA_EVAL_TILE=2048, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=6),
+    "e_t512_s4_m8": dict(GNA_EVAL_TILE=512, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=8, GNA_EVAL_THREADS=128),
+    "e_t1k_s3_m4_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=10, GNA_EVAL_THREADS=128),
 }
 
 
@@ -31,7 +30,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_batch.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_eval_tma.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
