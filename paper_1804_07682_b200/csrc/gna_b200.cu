@@ -110,13 +110,13 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
 #define GNA_EVAL_TILE 1024
 #endif
 #ifndef GNA_EVAL_STAGES
-#define GNA_EVAL_STAGES 3
+#define GNA_EVAL_STAGES 4
 #endif
 #ifndef GNA_EVAL_MINB
-#define GNA_EVAL_MINB 8
+#define GNA_EVAL_MINB 6
 #endif
 #ifndef GNA_EVAL_THREADS
-#define GNA_EVAL_THREADS 256
+#define GNA_EVAL_THREADS 128
 #endif
 constexpr int kEvalTile = GNA_EVAL_TILE;  // doubles per tile (8 KiB)
 constexpr int kEvalStages = GNA_EVAL_STAGES;
@@ -624,7 +624,7 @@ int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStr
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
   if (vec && n >= (int64_t)kEvalTile * 4) {
-    // persistent TMA-fed stream: GNA_EVAL_MINB blocks per SM (3 x 8 KiB smem ring each)
+    // persistent TMA-fed stream: GNA_EVAL_MINB blocks per SM (4 x 8 KiB smem ring each)
     const int64_t ntiles = n / kEvalTile;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * GNA_EVAL_MINB);
     k_oscprob_eval_tma<<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);

@@ -12,12 +12,12 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "e_t1k_s3_m8": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=8),
-    "e_t1k_s4_m6": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=6),
-    "e_t1k_s3_m6": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=6),
-    "e_t2k_s2_m6": dict(GNA_EVAL_TILE=2048, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=6),
-    "e_t512_s4_m8": dict(GNA_EVAL_TILE=512, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=8, GNA_EVAL_THREADS=128),
-    "e_t1k_s3_m4_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=10, GNA_EVAL_THREADS=128),
+    "e_t1k_s4_m6_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=6, GNA_EVAL_THREADS=128),
+    "e_t1k_s3_m8_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=8, GNA_EVAL_THREADS=128),
+    "e_t1k_s5_m5_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5, GNA_EVAL_THREADS=128),
+    "e_t2k_s2_m6_t128": dict(GNA_EVAL_TILE=2048, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=6, GNA_EVAL_THREADS=128),
+    "e_t1k_s4_m7_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=7, GNA_EVAL_THREADS=128),
+    "e_t1k_s2_m10_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=10, GNA_EVAL_THREADS=128),
 }
 
 
