@@ -474,6 +474,11 @@ def main():
                 "ops_per_energy_point": FP64_OPS_PER_EVAL,
                 "kernel_ms_per_launch": kern_avg_ms}
 
+    tr = _ncu_traffic(args.workload)
+    if tr:
+        roof["traffic"] = tr["bytes"]
+        roof["traffic_source"] = tr["source"]
+        roof["algorithmic_bytes"] = tr["algorithmic_bytes"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if scaling == "strong" else "weak",
@@ -497,6 +502,14 @@ def main():
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
+
+
+def _ncu_traffic(workload: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(workload)
+    except (OSError, ValueError):
+        return None
 
 
 def _smi_index(local: int) -> int:
