@@ -51,7 +51,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "cfg2", "cfg1"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "cfg2", "cfg1",
+                                                            "cfg4grid"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunks", type=int, default=0, help="gather pipeline chunks (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -76,6 +77,18 @@ def workload(name: str) -> dict:
                          "(%d bins x GL%d), spectra + chi2 per point" % (
                              name, c["L_km"].size, P, nb * c["order"], nb, c["order"]),
                          points=P, baselines=int(c["L_km"].size), bins=nb, order=c["order"])
+    elif name == "cfg4grid":
+        nmix, nmass = c["grid"]["theta12"].size, c["grid"]["dm2_21"].size
+        nb = c["edges"].size - 1
+        c["evals"] = nmix * nmass * c["L_km"].size * nb * c["order"]
+        c["bins_total"] = nmix * nmass * nb
+        c["points"] = synth.expand_grid(c["grid"])
+        c["desc"] = dict(workload="cfg4grid: %d x %d (theta13 x dm2_31) grid x %d energies "
+                         "(%d bins x GL%d) via the separable scan (NEXT-1); energy points = "
+                         "point x energy evaluations delivered" % (nmix, nmass, nb * c["order"],
+                                                                  nb, c["order"]),
+                         points=nmix * nmass, baselines=int(c["L_km"].size), bins=nb,
+                         order=c["order"])
     elif name == "cfg1":
         nb = c["edges"].size - 1
         c["evals"] = c["E"].size + nb * c["order"]
@@ -187,7 +200,7 @@ def run_reference(args, rank, world):
 
     def one_step():
         t0 = time.perf_counter()
-        if args.workload in ("cfg4", "cfg5"):
+        if args.workload in ("cfg4", "cfg5", "cfg4grid"):
             idx = np.arange(ns)
             sub = synth.subset_points(c["points"], idx)
             oracle.batch(sub, c["L_km"], c["omega"], c["edges"], c["order"], data=c["data"],
@@ -208,12 +221,12 @@ def run_reference(args, rank, world):
         return time.perf_counter() - t0, u
 
     # size each step to ~ (cpu_seconds / (steps+warmup)), bounded by the workload
-    ns = nt if args.workload in ("cfg4", "cfg5") else 10_000
+    ns = nt if args.workload in ("cfg4", "cfg5", "cfg4grid") else 10_000
     dt, u = one_step()
     rate = u / max(dt, 1e-9)
     per_step = max(0.05, min(args.cpu_seconds, 120.0) / max(args.steps + args.warmup, 1))
     full = {"cfg4": 10_000, "cfg5": 1000, "cfg2": 100_000, "cfg3": 100_000_000,
-            "cfg1": 100}[args.workload]
+            "cfg1": 100, "cfg4grid": 10_000}[args.workload]
     unit_per = u / ns
     ns = int(max(1, min(full, rate * per_step / unit_per)))
     for _ in range(args.warmup):
@@ -224,7 +237,7 @@ def run_reference(args, rank, world):
         units.append(u)
     value = sum(units) / sum(times)
     sample = "%d of %d %s per step (%s), oracle general complex formula, %d OpenMP threads" % (
-        ns, full, "parameter points" if args.workload in ("cfg4", "cfg5") else
+        ns, full, "parameter points" if args.workload in ("cfg4", "cfg5", "cfg4grid") else
         ("bins" if args.workload == "cfg2" else "energies"), args.workload, nt)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -242,7 +255,7 @@ def cpu_baseline(c, name, seconds):
     """The oracle as it stands, on a bounded sample of the same workload (rank 0, N=1)."""
     import oracle
     nt = oracle.max_threads()
-    if name in ("cfg4", "cfg5"):
+    if name in ("cfg4", "cfg5", "cfg4grid"):
         per_point = c["L_km"].size * (c["edges"].size - 1) * c["order"]
         P = c["points"]["theta12"].size
         n = min(P, nt)  # calibrate with one point per thread (the oracle threads over points)
@@ -343,6 +356,27 @@ def main():
         units_per_rank = (hi - lo) * L.size * nb * c["order"]
         calls_per_step = len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
         scaling = "strong"
+    elif args.workload == "cfg4grid":
+        grid = {k: torch.tensor(v, **f64) for k, v in c["grid"].items()}
+        edges = torch.tensor(c["edges"], **f64)
+        data = torch.tensor(c["data"], **f64)
+        nmix, nmass = c["grid"]["theta12"].size, c["grid"]["dm2_21"].size
+        nb = c["edges"].size - 1
+        sp_out = torch.empty((nmass, nmix, nb), **f64)
+        x2_out = torch.empty((nmass, nmix), **f64)
+        wsz = gna.oscprob_scan_workspace_size(nmix, nmass, nb) // 8 + 8
+        ws_raw = torch.empty(wsz, **f64)
+        ws = ws_raw[(-ws_raw.data_ptr()) % 32 // 8:]
+        kern_ev = []
+
+        def step():
+            with KernelTimer(kern_ev):
+                gna.oscprob_scan(grid, c["L_km"], c["omega"], edges, c["order"], data=data,
+                                 spectra=sp_out, chi2=x2_out, workspace=ws)
+
+        units_per_rank = c["evals"]
+        calls_per_step = 1
+        scaling = "weak"  # replicas only (one grid per GPU)
     elif args.workload == "cfg1":
         edges = torch.tensor(c["edges"], **f64)
         out = torch.empty(c["edges"].size - 1, **f64)
@@ -453,7 +487,17 @@ def main():
 
     # ---------------- roofline of the dominant kernel (batch / gl / eval)
     peak_ops = SM_COUNT * FP64_LANES_PER_SM * (clk.summary()["sm_max_mhz"] or 1965.0) * 1e6
-    if args.workload == "cfg3":
+    if args.workload == "cfg4grid":
+        # separable scan: the step is bound by writing the spectra (8 B per point x bin)
+        out_bytes = c["bins_total"] * 8
+        achieved = out_bytes / (kern_avg_ms * 1e-3) / 1e9
+        peaks = _measured_peaks()
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": peaks["source"],
+                "note": "whole gna_oscprob_scan call (stage-A sin^2 tables + rank-3 expansion "
+                        "+ chi2 reduce); algorithmic bytes = spectra written"}
+    elif args.workload == "cfg3":
         # co-limited stream: report the HBM side (16 B per energy) and note FP64
         launch_units = units_per_rank
         achieved = launch_units * 16 / (kern_avg_ms * 1e-3) / 1e9
@@ -492,8 +536,11 @@ def main():
             "cuda_graph": bool(use_graph)}
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
-    if not args.no_e2e:
+    if not args.no_e2e and args.workload != "cfg4grid":
         line["e2e"] = e2e(args, c, gna, torch, dist, dev, world, rank, local)
+    elif args.workload == "cfg4grid":
+        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0, "note": "no host-buffer variant of the scan yet"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c, args.workload, args.cpu_seconds)

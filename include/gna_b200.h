@@ -145,6 +145,41 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
                       void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gna_oscprob_scan — separable grid scan (the paper's
+ * "computed only once ... re-computed only if any of the variables or inputs it
+ * depends on were modified", and one transformation per formula item,
+ * P:641-642).  The parameter points are the grid {mixing point a} x {mass point c}:
+ *   point p = c * nmix + a  <->  (theta12[a], theta13[a], dm2_21[c], dm2_31[c]).
+ * The result is the same quantity as gna_oscprob_batch on that expanded list of
+ * points (same tolerance, different association): with
+ *   G[c][ij][k] = sum_b omega_b h_k sum_i w_i sin^2 Delta_ij(c, b, E_ki),
+ *   H[k] = (sum_b omega_b) h_k sum_i w_i,
+ *   T[p][k] = H[k] - sum_ij w_ij(a) G[c][ij][k],  chi2[p] as for the batch,
+ * the sin^2 work scales with nmass instead of nmass * nmix; the rest is a rank-3
+ * update per point, bound by writing the spectra.
+ * g: host struct of DEVICE arrays theta12/theta13 [nmix], dm2_21/dm2_31 [nmass].
+ * d_spectra: device [nmass][nmix][nbins] or NULL; d_chi2: device [nmass][nmix] or
+ * NULL (not both); d_data as for the batch.  d_workspace: device, 32-byte aligned,
+ * >= gna_oscprob_scan_workspace_size(nmix, nmass, nbins) bytes.  L_km/omega/nbase/
+ * d_edges/nbins/order and errors as for gna_oscprob_batch.
+ * ------------------------------------------------------------------------- */
+typedef struct gna_scan_grid {
+  const double* theta12;
+  const double* theta13;
+  int64_t nmix;
+  const double* dm2_21;
+  const double* dm2_31;
+  int64_t nmass;
+} gna_scan_grid;
+
+size_t gna_oscprob_scan_workspace_size(int64_t nmix, int64_t nmass, int64_t nbins);
+
+int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
+                     int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                     double* d_spectra, const double* d_data, double* d_chi2, void* d_workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Host-buffer variants (the end-to-end path; §4.1 "CUDA Streams,
  * datasets are divided into smaller sizes to organize overlapped execution,
  * asynchronous memory copying").  Same arithmetic as the device entry points

@@ -25,6 +25,7 @@ __all__ = [
     "oscprob_batch_workspace_size", "oscprob_eval_host", "gl_integrate_host",
     "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
+    "oscprob_scan", "oscprob_scan_workspace_size",
 ]
 
 GNA_OK, GNA_EINVAL, GNA_ECUDA, GNA_ENODEV, GNA_ENOMEM = 0, -1, -2, -3, -4
@@ -37,6 +38,7 @@ EXPORTS = (
     "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_gl_integrate_host",
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
+    "gna_oscprob_scan_workspace_size", "gna_oscprob_scan",
 )
 
 
@@ -54,6 +56,12 @@ class _CParams(ctypes.Structure):
                 ("theta23", ctypes.c_double), ("delta_cp", ctypes.c_double),
                 ("dm2_21", ctypes.c_double), ("dm2_31", ctypes.c_double),
                 ("antineutrino", ctypes.c_int32)]
+
+
+class _CScan(ctypes.Structure):
+    _fields_ = [("theta12", ctypes.c_void_p), ("theta13", ctypes.c_void_p),
+                ("nmix", ctypes.c_int64), ("dm2_21", ctypes.c_void_p),
+                ("dm2_31", ctypes.c_void_p), ("nmass", ctypes.c_int64)]
 
 
 class _CBatch(ctypes.Structure):
@@ -111,6 +119,11 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_oscprob_eval_host.argtypes = [P, d, vp, i64, vp, i64, vp]
     L.gna_oscprob_batch_host.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, i64, vp]
     L.gna_gl_integrate_host.argtypes = [P, d, vp, i64, i32, vp, i64, vp]
+    S = ctypes.POINTER(_CScan)
+    L.gna_oscprob_scan_workspace_size.argtypes = [i64, i64, i64]
+    L.gna_oscprob_scan_workspace_size.restype = sz
+    L.gna_oscprob_scan.argtypes = [S, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
+    L.gna_oscprob_scan.restype = ctypes.c_int
     L.gna_release.argtypes = []
     L.gna_release.restype = None
     L.gna_gl_rule.argtypes = [i32, vp, vp]
@@ -234,6 +247,48 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
         _dev(chi2, "chi2", P) if chi2 is not None else None,
         _dev(workspace, "workspace"), workspace.numel() * 8, _stream(stream)),
         "gna_oscprob_batch")
+    return spectra, chi2
+
+
+def oscprob_scan_workspace_size(nmix: int, nmass: int, nbins: int) -> int:
+    return int(load().gna_oscprob_scan_workspace_size(int(nmix), int(nmass), int(nbins)))
+
+
+def oscprob_scan(grid: dict, L_km, omega, edges, order: int, data=None, spectra=True, chi2=None,
+                 workspace=None, stream=None):
+    """Separable grid scan (gna_oscprob_scan): mixing points theta12/theta13 [nmix] x
+    mass points dm2_21/dm2_31 [nmass] (CUDA float64 tensors).  Returns (spectra
+    [nmass, nmix, nbins] or None, chi2 [nmass, nmix] or None)."""
+    import torch
+    L = load()
+    nmix = grid["theta12"].numel()
+    nmass = grid["dm2_21"].numel()
+    nbins = edges.numel() - 1
+    dev = edges.device
+    if spectra is True:
+        spectra = torch.empty((nmass, nmix, max(nbins, 0)), dtype=torch.float64, device=dev)
+    elif spectra is False:
+        spectra = None
+    if data is not None and chi2 is None:
+        chi2 = torch.empty((nmass, nmix), dtype=torch.float64, device=dev)
+    if workspace is None:
+        wb = oscprob_scan_workspace_size(nmix, nmass, nbins)
+        workspace = torch.empty(max(wb // 8, 4) + 4, dtype=torch.float64, device=dev)
+        off = (-workspace.data_ptr()) % 32 // 8  # 32-byte alignment
+        workspace = workspace[off:]
+    g = _CScan(_dev(grid["theta12"], "theta12", nmix), _dev(grid["theta13"], "theta13", nmix),
+               nmix, _dev(grid["dm2_21"], "dm2_21", nmass), _dev(grid["dm2_31"], "dm2_31", nmass),
+               nmass)
+    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    if Lh.size != om.size:
+        raise ValueError("L_km and omega must have the same length")
+    _check(L.gna_oscprob_scan(
+        ctypes.byref(g), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins,
+        int(order),
+        _dev(spectra, "spectra", nmass * nmix * nbins) if spectra is not None else None,
+        _dev(data, "data", nbins) if data is not None else None,
+        _dev(chi2, "chi2", nmass * nmix) if chi2 is not None else None,
+        workspace.data_ptr(), workspace.numel() * 8, _stream(stream)), "gna_oscprob_scan")
     return spectra, chi2
 
 

@@ -237,6 +237,7 @@ struct BatchWs {
 };
 
 size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+size_t align32(size_t x) { return (x + 31) & ~(size_t)31; }
 
 int64_t warps_per_point(int64_t nbins) { return (nbins + 31) / 32; }
 
@@ -414,6 +415,141 @@ __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __
 }
 
 // ----------------------------------------------------------------------------
+// NEXT-1: separable grid scan ("computed only once ... re-computed
+// only if any of the variables or inputs it depends on were modified", P:641-642 one
+// transformation per formula item).  The mixing weights enter P_ee only linearly, so for a
+// grid {mixing points a} x {mass points c} the binned sin^2 sums depend on c alone:
+//   G[c][ij][k] = sum_b omega_b h_k sum_i w_i sin^2(Delta_ij(c, b, E_ki)),
+//   H[k]        = Omega h_k sum_i w_i,
+//   T[c*nmix+a][k] = H[k] - sum_ij w_ij(a) G[c][ij][k]      (a rank-3 update per point).
+// Stage A costs nmass x nbase x 3 x nbins x order sin^2 (FP64); stage B is bound by writing
+// the spectra to HBM.
+struct ScanArgs {
+  double L[GNA_MAX_NBASE];
+  double omega[GNA_MAX_NBASE];
+  double omega_sum;
+  int nbase;
+  int order;
+  int64_t nbins;
+  int64_t nmix;
+  int64_t nmass;
+};
+
+struct ScanWs {
+  double* G;        // [nmass][3][nbins]
+  double* H;        // [nbins]
+  double* wmix;     // [nmix][4]  (w21, w31, w32, 0)
+  double* partial;  // [nmass*nmix][wpp]
+};
+
+size_t scan_ws_bytes(int64_t nmix, int64_t nmass, int64_t nbins, bool chi2) {
+  size_t b = align32((size_t)nmass * 3 * nbins * sizeof(double));
+  b += align32((size_t)nbins * sizeof(double));
+  b += align32((size_t)nmix * 4 * sizeof(double));
+  if (chi2) b += align32((size_t)nmass * nmix * warps_per_point(nbins) * sizeof(double));
+  return b;
+}
+
+ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins, bool chi2) {
+  char* c = (char*)base;
+  ScanWs w;
+  w.G = (double*)c;
+  c += align32((size_t)nmass * 3 * nbins * sizeof(double));
+  w.H = (double*)c;
+  c += align32((size_t)nbins * sizeof(double));
+  w.wmix = (double*)c;
+  c += align32((size_t)nmix * 4 * sizeof(double));
+  w.partial = chi2 ? (double*)c : nullptr;
+  return w;
+}
+
+// stage A: thread per (mass point c, bin k) -> G[c][*][k] (and H[k] for c == 0);
+// extra threads compute the mixing weights of each mixing point.
+__global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
+                                                    const double* __restrict__ th13,
+                                                    const double* __restrict__ d21,
+                                                    const double* __restrict__ d31,
+                                                    const double* __restrict__ edges, ScanWs w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = a.nmass * a.nbins;
+  if (t < n1) {
+    const int64_t c = t / a.nbins;
+    const int64_t k = t - c * a.nbins;
+    const int off = GNA_GL_OFF(a.order);
+    const double e0 = edges[k], e1 = edges[k + 1];
+    const double ctr = 0.5 * (e0 + e1);
+    const double h = 0.5 * (e1 - e0);
+    double wsum = 0.0;
+    for (int i = 0; i < a.order; ++i) wsum += c_gl_w[off + i];
+    const double m21 = d21[c], m31 = d31[c];
+    const double m[3] = {m21, m31, m31 - m21};
+    double G[3] = {0.0, 0.0, 0.0};
+    for (int b = 0; b < a.nbase; ++b) {
+      const double kq0 = phase_slope(m[0], a.L[b]);
+      const double kq1 = phase_slope(m[1], a.L[b]);
+      const double kq2 = phase_slope(m[2], a.L[b]);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int i = 0; i < a.order; ++i) {
+        const double invE = 1.0 / fma(h, c_gl_t[off + i], ctr);
+        const double wi = c_gl_w[off + i];
+        s0 = fma(wi, gna::sin2c(kq0, invE), s0);
+        s1 = fma(wi, gna::sin2c(kq1, invE), s1);
+        s2 = fma(wi, gna::sin2c(kq2, invE), s2);
+      }
+      // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
+      const double ob = a.omega[b] * h;
+      G[0] = fma(ob, fma(0.5, wsum, s0), G[0]);
+      G[1] = fma(ob, fma(0.5, wsum, s1), G[1]);
+      G[2] = fma(ob, fma(0.5, wsum, s2), G[2]);
+    }
+    double* g = w.G + (c * 3) * a.nbins + k;
+    g[0] = G[0];
+    g[a.nbins] = G[1];
+    g[2 * a.nbins] = G[2];
+    if (c == 0) w.H[k] = a.omega_sum * h * wsum;
+  } else if (t < n1 + a.nmix) {
+    const int64_t m = t - n1;
+    double s12, c12, s13, c13;
+    sincos(th12[m], &s12, &c12);
+    sincos(th13[m], &s13, &c13);
+    double* wm = w.wmix + 4 * m;
+    mixing_weights(s12, c12, s13, c13, &wm[0], &wm[1], &wm[2]);
+    wm[3] = 0.0;
+  }
+}
+
+// stage B: block = (point p = c*nmix + a, 256 consecutive bins); thread per output bin.
+constexpr int kScanThreads = 256;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int64_t nbins,
+                                                              int64_t bpp, ScanWs w,
+                                                              double* __restrict__ spectra,
+                                                              const double* __restrict__ data) {
+  const int64_t p = blockIdx.x / bpp;
+  const int64_t k = (blockIdx.x - p * bpp) * kScanThreads + threadIdx.x;
+  const int64_t c = p / nmix, a = p - c * nmix;
+  const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * a);
+  double x2 = 0.0;
+  if (k < nbins) {
+    const double* g = w.G + (c * 3) * nbins + k;
+    const double T = w.H[k] - fma(wm.x, g[0], fma(wm.y, g[nbins], wm.z * g[2 * nbins]));
+    if (spectra) __stcs(spectra + p * nbins + k, T);
+    if (data) {
+      const double D = data[k];
+      const double d = T - D;
+      x2 = d * d / D;
+    }
+  }
+  if (w.partial) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+    const int64_t wt = k >> 5;
+    if ((threadIdx.x & 31) == 0 && (wt << 5) < nbins)
+      w.partial[p * warps_per_point_dev(nbins) + wt] = x2;
+  }
+}
+
+// ----------------------------------------------------------------------------
 // host helpers
 // ----------------------------------------------------------------------------
 int cuda_fail(cudaError_t e) {
@@ -421,11 +557,11 @@ int cuda_fail(cudaError_t e) {
   return GNA_ECUDA;
 }
 
-bool finite(double x) { return std::isfinite(x); }
+bool is_fin(double x) { return std::isfinite(x); }
 
 bool params_ok(const gna_osc_params* p) {
-  return p && finite(p->theta12) && finite(p->theta13) && finite(p->theta23) &&
-         finite(p->delta_cp) && finite(p->dm2_21) && finite(p->dm2_31);
+  return p && is_fin(p->theta12) && is_fin(p->theta13) && is_fin(p->theta23) &&
+         is_fin(p->delta_cp) && is_fin(p->dm2_21) && is_fin(p->dm2_31);
 }
 
 bool overlap(const void* a, size_t na, const void* b, size_t nb) {
@@ -501,7 +637,7 @@ int sm_count() {
 
 // --- validation shared by device and host variants --------------------------
 int validate_eval(const gna_osc_params* p, double L_km, const double* E, int64_t n, const double* P) {
-  if (!params_ok(p) || !E || !P || n < 1 || !finite(L_km) || L_km < 0) return GNA_EINVAL;
+  if (!params_ok(p) || !E || !P || n < 1 || !is_fin(L_km) || L_km < 0) return GNA_EINVAL;
   if (overlap(E, (size_t)n * 8, P, (size_t)n * 8)) return GNA_EINVAL;
   return GNA_OK;
 }
@@ -509,7 +645,7 @@ int validate_eval(const gna_osc_params* p, double L_km, const double* E, int64_t
 int validate_gl(const gna_osc_params* p, double L_km, const double* edges, int64_t nbins,
                 int32_t order, const double* bins) {
   if (!params_ok(p) || !edges || !bins || nbins < 1 || order < 1 || order > GNA_MAX_ORDER ||
-      !finite(L_km) || L_km < 0)
+      !is_fin(L_km) || L_km < 0)
     return GNA_EINVAL;
   if (overlap(edges, (size_t)(nbins + 1) * 8, bins, (size_t)nbins * 8)) return GNA_EINVAL;
   return GNA_OK;
@@ -525,7 +661,7 @@ int validate_batch(const gna_param_batch* pts, const double* L_km, const double*
   if (!spectra && !chi2) return GNA_EINVAL;
   if (chi2 && !data) return GNA_EINVAL;
   for (int b = 0; b < nbase; ++b)
-    if (!finite(L_km[b]) || L_km[b] < 0 || !finite(omega[b])) return GNA_EINVAL;
+    if (!is_fin(L_km[b]) || L_km[b] < 0 || !is_fin(omega[b])) return GNA_EINVAL;
   const size_t P8 = (size_t)pts->npoints * 8;
   if (spectra) {
     const size_t S8 = (size_t)pts->npoints * (size_t)nbins * 8;
@@ -602,6 +738,49 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
     const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
     k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints, warps_per_point(nbins),
                                                   chi2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return GNA_OK;
+}
+
+int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega, int32_t nbase,
+                const double* edges, int64_t nbins, int32_t order, double* spectra,
+                const double* data, double* chi2, void* workspace, cudaStream_t s) {
+  ScanArgs a;
+  std::memset(&a, 0, sizeof(a));
+  double om = 0.0;
+  for (int b = 0; b < nbase; ++b) {
+    a.L[b] = L_km[b];
+    a.omega[b] = omega[b];
+    om += omega[b];
+  }
+  a.omega_sum = om;
+  a.nbase = nbase;
+  a.order = order;
+  a.nbins = nbins;
+  a.nmix = g->nmix;
+  a.nmass = g->nmass;
+  const ScanWs w = scan_ws_carve(workspace, g->nmix, g->nmass, nbins, chi2 != nullptr);
+  const int64_t nsetup = g->nmass * nbins + g->nmix;
+  const int64_t npts = g->nmass * g->nmix;
+  const int64_t bpp = (nbins + kScanThreads - 1) / kScanThreads;
+  if ((nsetup + 127) / 128 > 0x7fffffffLL || npts * bpp > 0x7fffffffLL) return GNA_EINVAL;
+  k_scan_setup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(a, g->theta12, g->theta13,
+                                                                g->dm2_21, g->dm2_31, edges, w);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  k_scan_expand<<<(unsigned)(npts * bpp), kScanThreads, 0, s>>>(g->nmix, nbins, bpp, w, spectra,
+                                                                chi2 ? data : nullptr);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (chi2) {
+    const int64_t threads = npts * 32;
+    const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
+    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(w.partial, npts, warps_per_point(nbins), chi2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
@@ -792,6 +971,41 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
                       d_workspace, (cudaStream_t)stream);
+}
+
+size_t gna_oscprob_scan_workspace_size(int64_t nmix, int64_t nmass, int64_t nbins) {
+  if (nmix < 1 || nmass < 1 || nbins < 1) return 0;
+  return scan_ws_bytes(nmix, nmass, nbins, true);
+}
+
+int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
+                     int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                     double* d_spectra, const double* d_data, double* d_chi2, void* d_workspace,
+                     size_t workspace_bytes, void* stream) {
+  if (!g || !g->theta12 || !g->theta13 || !g->dm2_21 || !g->dm2_31 || g->nmix < 1 ||
+      g->nmass < 1 || !L_km || !omega || nbase < 1 || nbase > GNA_MAX_NBASE || !d_edges ||
+      nbins < 1 || order < 1 || order > GNA_MAX_ORDER || (!d_spectra && !d_chi2) ||
+      (d_chi2 && !d_data) || !d_workspace || ((uintptr_t)d_workspace & 31))
+    return GNA_EINVAL;
+  for (int b = 0; b < nbase; ++b)
+    if (!is_fin(L_km[b]) || L_km[b] < 0 || !is_fin(omega[b])) return GNA_EINVAL;
+  const size_t W = scan_ws_bytes(g->nmix, g->nmass, nbins, d_chi2 != nullptr);
+  if (workspace_bytes < W) return GNA_EINVAL;
+  const size_t P8 = (size_t)g->nmass * g->nmix * 8;
+  const void* ins[9] = {g->theta12, g->theta13, g->dm2_21, g->dm2_31, d_edges, d_data,
+                        d_spectra, d_chi2, d_workspace};
+  const size_t ln[9] = {(size_t)g->nmix * 8, (size_t)g->nmix * 8, (size_t)g->nmass * 8,
+                        (size_t)g->nmass * 8, (size_t)(nbins + 1) * 8, (size_t)nbins * 8,
+                        P8 * (size_t)nbins, P8, W};
+  for (int i = 5; i < 9; ++i)  // outputs and workspace vs everything else
+    for (int j = 0; j < 9; ++j)
+      if (i != j && ins[i] && ins[j] && overlap(ins[i], ln[i], ins[j], ln[j])) return GNA_EINVAL;
+  int rc;
+  if ((rc = check_device())) return rc;
+  for (const void* q : ins)
+    if (q && check_dev_ptr(q)) return GNA_EINVAL;
+  return launch_scan(g, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
+                     d_workspace, (cudaStream_t)stream);
 }
 
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,

@@ -105,7 +105,27 @@ def config(name: str) -> dict:
         omega = (L_JUNO / L) ** 2
         return dict(name=name, points=pts, L_km=L, omega=omega, edges=edges, order=10,
                     data=pseudo_data(g, edges, float(omega.sum())))
+    if name == "cfg4grid":
+        # the cfg4 scan as a structured 100 x 100 grid (SURVEY §8(d) "secondary"): mixing
+        # points (theta13) x mass points (dm2_31); the separable path (NEXT-1) runs it
+        n13, n31 = 100, 100
+        grid = dict(theta12=np.full(n13, CANONICAL["theta12"]),
+                    theta13=np.linspace(0.10, 0.20, n13),
+                    dm2_21=np.full(n31, CANONICAL["dm2_21"]),
+                    dm2_31=np.linspace(2.3e-3, 2.7e-3, n31))
+        edges = uniform_edges(1000)
+        L = np.array([L_JUNO])
+        omega = np.array([1.0])
+        return dict(name=name, grid=grid, L_km=L, omega=omega, edges=edges, order=10,
+                    data=pseudo_data(g, edges, float(omega.sum())))
     raise KeyError(name)
+
+
+def expand_grid(grid: dict) -> dict:
+    """Point list of a separable grid in the scan's order: p = c * nmix + a."""
+    nmix, nmass = grid["theta12"].size, grid["dm2_21"].size
+    return dict(theta12=np.tile(grid["theta12"], nmass), theta13=np.tile(grid["theta13"], nmass),
+                dm2_21=np.repeat(grid["dm2_21"], nmix), dm2_31=np.repeat(grid["dm2_31"], nmix))
 
 
 def subset_points(points: dict, idx) -> dict:

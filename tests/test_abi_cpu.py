@@ -140,6 +140,39 @@ def test_batch_einval(lib, case):
         assert _batch(lib, host=True, **case) == gna.GNA_EINVAL
 
 
+def _scan(lib, **kw):
+    g = gna._CScan(0x100000, 0x200000, kw.get("nmix", 4), 0x300000, kw.get("d31", 0x400000),
+                   kw.get("nmass", 3))
+    nb = kw.get("nbase", 1)
+    L = np.full(max(nb, 1), kw.get("L", 52.5))
+    om = np.ones(max(nb, 1))
+    return lib.gna_oscprob_scan(ctypes.byref(g), L.ctypes.data, om.ctypes.data, nb,
+                                kw.get("edges", 0x500000), kw.get("nbins", 10),
+                                kw.get("order", 5), kw.get("spectra", 0x600000),
+                                kw.get("data", 0x700000), kw.get("chi2", 0x800000),
+                                kw.get("ws", 0x900000), kw.get("wsb", 1 << 20), None)
+
+
+@pytest.mark.parametrize("case", [
+    dict(nmix=0), dict(nmass=0), dict(nbase=0), dict(nbase=65), dict(nbins=0), dict(order=0),
+    dict(order=33), dict(spectra=None, chi2=None), dict(data=None), dict(edges=None),
+    dict(d31=None), dict(L=-1.0), dict(L=float("inf")), dict(ws=None), dict(wsb=64),
+    dict(ws=0x900010),                # not 32-byte aligned
+    dict(chi2=0x600000 + 8),          # chi2 inside spectra
+    dict(ws=0x100000 - 64),           # workspace overlaps theta12
+])
+def test_scan_einval(lib, case):
+    assert _scan(lib, **case) == gna.GNA_EINVAL
+
+
+def test_scan_workspace_size(lib):
+    assert gna.oscprob_scan_workspace_size(0, 1, 10) == 0
+    assert gna.oscprob_scan_workspace_size(1, 0, 10) == 0
+    assert gna.oscprob_scan_workspace_size(1, 1, 0) == 0
+    w = gna.oscprob_scan_workspace_size(100, 100, 1000)
+    assert w >= 100 * 3 * 1000 * 8 + 1000 * 8 + 100 * 32 + 10_000 * 32 * 8 and w % 32 == 0
+
+
 def test_batch_workspace_size(lib):
     assert gna.oscprob_batch_workspace_size(0, 1, 10, 5) == 0
     assert gna.oscprob_batch_workspace_size(10, 1, 0, 5) == 0

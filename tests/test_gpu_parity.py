@@ -255,6 +255,51 @@ def test_batch_cfg5_full_size_sampled_and_split_invariant(gna):
         assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi])
 
 
+# ------------------------------------------------------------------------ NEXT-1 separable scan
+def _scan_case(g, nmix, nmass, nbase, nbins, order):
+    grid = dict(theta12=g.uniform(0.5, 0.65, nmix), theta13=g.uniform(0.1, 0.2, nmix),
+                dm2_21=g.uniform(6e-5, 9e-5, nmass), dm2_31=g.uniform(2.2e-3, 2.8e-3, nmass))
+    L = g.uniform(1.0, 300.0, nbase)
+    om = g.uniform(0.1, 2.0, nbase)
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    data = synth.pseudo_data(g, edges, om.sum())
+    return grid, L, om, edges, data
+
+
+@pytest.mark.parametrize("nmix,nmass,nbase,nbins,order", [
+    (1, 1, 1, 1, 1), (7, 5, 3, 37, 4), (3, 4, 8, 300, 10), (2, 2, 64, 50, 32), (33, 1, 1, 257, 5)])
+def test_scan_vs_oracle_on_expanded_grid(gna, nmix, nmass, nbase, nbins, order):
+    g = synth.rng(500 + nmix * nmass + nbins)
+    grid, L, om, edges, data = _scan_case(g, nmix, nmass, nbase, nbins, order)
+    sp, x2 = gna.oscprob_scan({k: _t(v) for k, v in grid.items()}, L, om, _t(edges), order,
+                              data=_t(data))
+    sp, x2 = _np(sp).reshape(nmass * nmix, nbins), _np(x2).ravel()
+    spr, x2r = oracle.batch(synth.expand_grid(grid), L, om, edges, order, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sp - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2 - x2r) <= _chi2_bound(spr, data))
+    # same quantity as the per-point batch path on the expanded points
+    spb, x2b = _run_batch(gna, synth.expand_grid(grid), L, om, edges, order, data)
+    assert np.max(np.abs(sp - spb) / np.abs(spb)) <= 1e-13
+
+
+def test_scan_cfg4grid_full_size_sampled(gna):
+    c = synth.config("cfg4grid")
+    sp, x2 = gna.oscprob_scan({k: _t(v) for k, v in c["grid"].items()}, c["L_km"], c["omega"],
+                              _t(c["edges"]), c["order"], data=_t(c["data"]))
+    sp, x2 = _np(sp).reshape(-1, c["edges"].size - 1), _np(x2).ravel()
+    pts = synth.expand_grid(c["grid"])
+    idx = np.array([0, 1, 99, 100, 5050, 9999])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), c["L_km"], c["omega"], c["edges"],
+                            c["order"], data=c["data"], nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, c["data"]))
+    # chi2-only run gives the same bits
+    _, x2o = gna.oscprob_scan({k: _t(v) for k, v in c["grid"].items()}, c["L_km"], c["omega"],
+                              _t(c["edges"]), c["order"], data=_t(c["data"]), spectra=False)
+    assert np.array_equal(_np(x2o).ravel(), x2)
+
+
 # ------------------------------------------------------------------------ host-buffer path
 def test_eval_host_bitwise_equals_device(gna):
     g = synth.rng(51)
