@@ -436,45 +436,48 @@ struct ScanArgs {
 };
 
 struct ScanWs {
-  double* G;        // [nmass][3][nbins]
-  double* H;        // [nbins]
-  double* wmix;     // [nmix][4]  (w21, w31, w32, 0)
-  double* partial;  // [nmass*nmix][wpp]
+  double* G;     // [nmass][3][nbins]
+  double* H;     // [nbins]
+  double* invD;  // [nbins]  1 / data (chi2 only)
+  double* wmix;  // [nmix][4]  (w21, w31, w32, 0)
 };
 
-size_t scan_ws_bytes(int64_t nmix, int64_t nmass, int64_t nbins, bool chi2) {
+size_t scan_ws_bytes(int64_t nmix, int64_t nmass, int64_t nbins) {
   size_t b = align32((size_t)nmass * 3 * nbins * sizeof(double));
-  b += align32((size_t)nbins * sizeof(double));
+  b += 2 * align32((size_t)nbins * sizeof(double));
   b += align32((size_t)nmix * 4 * sizeof(double));
-  if (chi2) b += align32((size_t)nmass * nmix * warps_per_point(nbins) * sizeof(double));
   return b;
 }
 
-ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins, bool chi2) {
+ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
   char* c = (char*)base;
   ScanWs w;
   w.G = (double*)c;
   c += align32((size_t)nmass * 3 * nbins * sizeof(double));
   w.H = (double*)c;
   c += align32((size_t)nbins * sizeof(double));
+  w.invD = (double*)c;
+  c += align32((size_t)nbins * sizeof(double));
   w.wmix = (double*)c;
-  c += align32((size_t)nmix * 4 * sizeof(double));
-  w.partial = chi2 ? (double*)c : nullptr;
   return w;
 }
 
-// stage A: thread per (mass point c, bin k) -> G[c][*][k] (and H[k] for c == 0);
-// extra threads compute the mixing weights of each mixing point.
+// stage A: thread per (mass point c, pair ij, bin k) -> G[c][ij][k]; threads with
+// c == 0, ij == 0 also write H[k] and 1/D[k]; extra threads compute the mixing
+// weights of each mixing point.
 __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
                                                     const double* __restrict__ th13,
                                                     const double* __restrict__ d21,
                                                     const double* __restrict__ d31,
-                                                    const double* __restrict__ edges, ScanWs w) {
+                                                    const double* __restrict__ edges,
+                                                    const double* __restrict__ data, ScanWs w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n1 = a.nmass * a.nbins;
+  const int64_t n1 = a.nmass * 3 * a.nbins;
   if (t < n1) {
-    const int64_t c = t / a.nbins;
-    const int64_t k = t - c * a.nbins;
+    const int64_t row = t / a.nbins;  // c * 3 + ij
+    const int64_t k = t - row * a.nbins;
+    const int64_t c = row / 3;
+    const int ij = (int)(row - c * 3);
     const int off = GNA_GL_OFF(a.order);
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
@@ -482,70 +485,69 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
     double wsum = 0.0;
     for (int i = 0; i < a.order; ++i) wsum += c_gl_w[off + i];
     const double m21 = d21[c], m31 = d31[c];
-    const double m[3] = {m21, m31, m31 - m21};
-    double G[3] = {0.0, 0.0, 0.0};
+    const double m = ij == 0 ? m21 : (ij == 1 ? m31 : m31 - m21);
+    double G = 0.0;
     for (int b = 0; b < a.nbase; ++b) {
-      const double kq0 = phase_slope(m[0], a.L[b]);
-      const double kq1 = phase_slope(m[1], a.L[b]);
-      const double kq2 = phase_slope(m[2], a.L[b]);
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int i = 0; i < a.order; ++i) {
-        const double invE = 1.0 / fma(h, c_gl_t[off + i], ctr);
-        const double wi = c_gl_w[off + i];
-        s0 = fma(wi, gna::sin2c(kq0, invE), s0);
-        s1 = fma(wi, gna::sin2c(kq1, invE), s1);
-        s2 = fma(wi, gna::sin2c(kq2, invE), s2);
-      }
+      const double kq = phase_slope(m, a.L[b]);
+      double s = 0.0;
+      for (int i = 0; i < a.order; ++i)
+        s = fma(c_gl_w[off + i], gna::sin2c(kq, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
       // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
-      const double ob = a.omega[b] * h;
-      G[0] = fma(ob, fma(0.5, wsum, s0), G[0]);
-      G[1] = fma(ob, fma(0.5, wsum, s1), G[1]);
-      G[2] = fma(ob, fma(0.5, wsum, s2), G[2]);
+      G = fma(a.omega[b] * h, fma(0.5, wsum, s), G);
     }
-    double* g = w.G + (c * 3) * a.nbins + k;
-    g[0] = G[0];
-    g[a.nbins] = G[1];
-    g[2 * a.nbins] = G[2];
-    if (c == 0) w.H[k] = a.omega_sum * h * wsum;
+    w.G[t] = G;
+    if (row == 0) {
+      w.H[k] = a.omega_sum * h * wsum;
+      if (data) w.invD[k] = 1.0 / data[k];
+    }
   } else if (t < n1 + a.nmix) {
-    const int64_t m = t - n1;
+    const int64_t mm = t - n1;
     double s12, c12, s13, c13;
-    sincos(th12[m], &s12, &c12);
-    sincos(th13[m], &s13, &c13);
-    double* wm = w.wmix + 4 * m;
+    sincos(th12[mm], &s12, &c12);
+    sincos(th13[mm], &s13, &c13);
+    double* wm = w.wmix + 4 * mm;
     mixing_weights(s12, c12, s13, c13, &wm[0], &wm[1], &wm[2]);
     wm[3] = 0.0;
   }
 }
 
-// stage B: block = (point p = c*nmix + a, 256 consecutive bins); thread per output bin.
+// stage B: block = point p = c*nmix + a, looping over its bins (no per-thread index
+// division); chi2 reduced in the block with a fixed shuffle tree + warps in order.
 constexpr int kScanThreads = 256;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int64_t nbins,
-                                                              int64_t bpp, ScanWs w,
+                                                              ScanWs w,
                                                               double* __restrict__ spectra,
-                                                              const double* __restrict__ data) {
-  const int64_t p = blockIdx.x / bpp;
-  const int64_t k = (blockIdx.x - p * bpp) * kScanThreads + threadIdx.x;
+                                                              const double* __restrict__ data,
+                                                              double* __restrict__ chi2) {
+  __shared__ double s_warp[kScanThreads / 32];
+  const int64_t p = blockIdx.x;
   const int64_t c = p / nmix, a = p - c * nmix;
   const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * a);
+  const double* __restrict__ g0 = w.G + (c * 3) * nbins;
+  const double* __restrict__ g1 = g0 + nbins;
+  const double* __restrict__ g2 = g1 + nbins;
+  double* __restrict__ out = spectra ? spectra + p * nbins : nullptr;
   double x2 = 0.0;
-  if (k < nbins) {
-    const double* g = w.G + (c * 3) * nbins + k;
-    const double T = w.H[k] - fma(wm.x, g[0], fma(wm.y, g[nbins], wm.z * g[2 * nbins]));
-    if (spectra) __stcs(spectra + p * nbins + k, T);
-    if (data) {
-      const double D = data[k];
-      const double d = T - D;
-      x2 = d * d / D;
+  for (int64_t k = threadIdx.x; k < nbins; k += kScanThreads) {
+    const double T = w.H[k] - fma(wm.x, g0[k], fma(wm.y, g1[k], wm.z * g2[k]));
+    if (out) __stcs(out + k, T);
+    if (chi2) {
+      const double d = T - data[k];
+      x2 = fma(d * d, w.invD[k], x2);
     }
   }
-  if (w.partial) {
+  if (chi2) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-    const int64_t wt = k >> 5;
-    if ((threadIdx.x & 31) == 0 && (wt << 5) < nbins)
-      w.partial[p * warps_per_point_dev(nbins) + wt] = x2;
+    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = x2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < kScanThreads / 32; ++i) t += s_warp[i];
+      chi2[p] = t;
+    }
   }
 }
 
@@ -762,30 +764,20 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   a.nbins = nbins;
   a.nmix = g->nmix;
   a.nmass = g->nmass;
-  const ScanWs w = scan_ws_carve(workspace, g->nmix, g->nmass, nbins, chi2 != nullptr);
-  const int64_t nsetup = g->nmass * nbins + g->nmix;
+  const ScanWs w = scan_ws_carve(workspace, g->nmix, g->nmass, nbins);
+  const int64_t nsetup = g->nmass * 3 * nbins + g->nmix;
   const int64_t npts = g->nmass * g->nmix;
-  const int64_t bpp = (nbins + kScanThreads - 1) / kScanThreads;
-  if ((nsetup + 127) / 128 > 0x7fffffffLL || npts * bpp > 0x7fffffffLL) return GNA_EINVAL;
-  k_scan_setup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(a, g->theta12, g->theta13,
-                                                                g->dm2_21, g->dm2_31, edges, w);
+  if ((nsetup + 127) / 128 > 0x7fffffffLL || npts > 0x7fffffffLL) return GNA_EINVAL;
+  k_scan_setup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
+      a, g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges, chi2 ? data : nullptr, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
-  k_scan_expand<<<(unsigned)(npts * bpp), kScanThreads, 0, s>>>(g->nmix, nbins, bpp, w, spectra,
-                                                                chi2 ? data : nullptr);
+  k_scan_expand<<<(unsigned)npts, kScanThreads, 0, s>>>(g->nmix, nbins, w, spectra,
+                                                        chi2 ? data : nullptr, chi2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
-  if (e != cudaSuccess) return cuda_fail(e);
-  if (chi2) {
-    const int64_t threads = npts * 32;
-    const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
-    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(w.partial, npts, warps_per_point(nbins), chi2);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e);
-  }
-  return GNA_OK;
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
 
 int launch_gl(const PeeCoef& c, const double* edges, int64_t nbins, int order, double* bins,
@@ -975,7 +967,7 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
 
 size_t gna_oscprob_scan_workspace_size(int64_t nmix, int64_t nmass, int64_t nbins) {
   if (nmix < 1 || nmass < 1 || nbins < 1) return 0;
-  return scan_ws_bytes(nmix, nmass, nbins, true);
+  return scan_ws_bytes(nmix, nmass, nbins);
 }
 
 int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
@@ -989,7 +981,7 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
     return GNA_EINVAL;
   for (int b = 0; b < nbase; ++b)
     if (!is_fin(L_km[b]) || L_km[b] < 0 || !is_fin(omega[b])) return GNA_EINVAL;
-  const size_t W = scan_ws_bytes(g->nmix, g->nmass, nbins, d_chi2 != nullptr);
+  const size_t W = scan_ws_bytes(g->nmix, g->nmass, nbins);
   if (workspace_bytes < W) return GNA_EINVAL;
   const size_t P8 = (size_t)g->nmass * g->nmix * 8;
   const void* ins[9] = {g->theta12, g->theta13, g->dm2_21, g->dm2_31, d_edges, d_data,
