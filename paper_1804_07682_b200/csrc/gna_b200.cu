@@ -511,42 +511,64 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
   }
 }
 
-// stage B: block = point p = c*nmix + a, looping over its bins (no per-thread index
-// division); chi2 reduced in the block with a fixed shuffle tree + warps in order.
+// stage B: block = (mass point c, chunk of kScanA mixing points).  Each thread loads
+// G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
+// (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
+// point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
 constexpr int kScanThreads = 256;
+constexpr int kScanA = 16;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int64_t nbins,
-                                                              ScanWs w,
+                                                              int64_t nchunk, ScanWs w,
                                                               double* __restrict__ spectra,
                                                               const double* __restrict__ data,
                                                               double* __restrict__ chi2) {
-  __shared__ double s_warp[kScanThreads / 32];
-  const int64_t p = blockIdx.x;
-  const int64_t c = p / nmix, a = p - c * nmix;
-  const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * a);
+  __shared__ double s_x2[kScanA][kScanThreads / 32];
+  const int64_t c = blockIdx.x / nchunk;
+  const int64_t a0 = (blockIdx.x - c * nchunk) * kScanA;
+  const int na = (int)min((int64_t)kScanA, nmix - a0);
+  double w0[kScanA], w1[kScanA], w2[kScanA], x2[kScanA];
+#pragma unroll
+  for (int j = 0; j < kScanA; ++j) {
+    const int64_t aj = a0 + (j < na ? j : 0);
+    const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * aj);
+    w0[j] = wm.x;
+    w1[j] = wm.y;
+    w2[j] = wm.z;
+    x2[j] = 0.0;
+  }
   const double* __restrict__ g0 = w.G + (c * 3) * nbins;
   const double* __restrict__ g1 = g0 + nbins;
   const double* __restrict__ g2 = g1 + nbins;
-  double* __restrict__ out = spectra ? spectra + p * nbins : nullptr;
-  double x2 = 0.0;
+  double* __restrict__ out = spectra ? spectra + (c * nmix + a0) * nbins : nullptr;
   for (int64_t k = threadIdx.x; k < nbins; k += kScanThreads) {
-    const double T = w.H[k] - fma(wm.x, g0[k], fma(wm.y, g1[k], wm.z * g2[k]));
-    if (out) __stcs(out + k, T);
-    if (chi2) {
-      const double d = T - data[k];
-      x2 = fma(d * d, w.invD[k], x2);
+    const double G0 = g0[k], G1 = g1[k], G2 = g2[k], H = w.H[k];
+    const double D = chi2 ? data[k] : 0.0, iD = chi2 ? w.invD[k] : 0.0;
+#pragma unroll
+    for (int j = 0; j < kScanA; ++j) {
+      if (j < na) {
+        const double T = H - fma(w0[j], G0, fma(w1[j], G1, w2[j] * G2));
+        if (out) __stcs(out + (int64_t)j * nbins + k, T);
+        const double d = T - D;
+        x2[j] = fma(d * d, iD, x2[j]);
+      }
     }
   }
   if (chi2) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-    if ((threadIdx.x & 31) == 0) s_warp[threadIdx.x >> 5] = x2;
+    for (int j = 0; j < kScanA; ++j) {
+      double v = x2[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s_x2[j][warp] = v;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < na) {
       double t = 0.0;
 #pragma unroll
-      for (int i = 0; i < kScanThreads / 32; ++i) t += s_warp[i];
-      chi2[p] = t;
+      for (int i = 0; i < kScanThreads / 32; ++i) t += s_x2[threadIdx.x][i];
+      chi2[c * nmix + a0 + threadIdx.x] = t;
     }
   }
 }
@@ -766,14 +788,15 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   a.nmass = g->nmass;
   const ScanWs w = scan_ws_carve(workspace, g->nmix, g->nmass, nbins);
   const int64_t nsetup = g->nmass * 3 * nbins + g->nmix;
-  const int64_t npts = g->nmass * g->nmix;
-  if ((nsetup + 127) / 128 > 0x7fffffffLL || npts > 0x7fffffffLL) return GNA_EINVAL;
+  const int64_t nchunk = (g->nmix + kScanA - 1) / kScanA;
+  const int64_t nblk = g->nmass * nchunk;
+  if ((nsetup + 127) / 128 > 0x7fffffffLL || nblk > 0x7fffffffLL) return GNA_EINVAL;
   k_scan_setup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
       a, g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges, chi2 ? data : nullptr, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
-  k_scan_expand<<<(unsigned)npts, kScanThreads, 0, s>>>(g->nmix, nbins, w, spectra,
+  k_scan_expand<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
                                                         chi2 ? data : nullptr, chi2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
