@@ -511,12 +511,18 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
   }
 }
 
-// stage B: block = (mass point c, chunk of kScanA mixing points).  Each thread loads
+// stage B: block = (mass point c, chunk of kScanA (8) mixing points).  Each thread loads
 // G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
 // (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
 // point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
-constexpr int kScanThreads = 256;
-constexpr int kScanA = 16;
+#ifndef GNA_SCAN_A
+#define GNA_SCAN_A 8
+#endif
+#ifndef GNA_SCAN_THREADS
+#define GNA_SCAN_THREADS 256
+#endif
+constexpr int kScanThreads = GNA_SCAN_THREADS;
+constexpr int kScanA = GNA_SCAN_A;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int64_t nbins,
                                                               int64_t nchunk, ScanWs w,

@@ -12,12 +12,12 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "e_t1k_s4_m6_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=6, GNA_EVAL_THREADS=128),
-    "e_t1k_s3_m8_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=3, GNA_EVAL_MINB=8, GNA_EVAL_THREADS=128),
-    "e_t1k_s5_m5_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5, GNA_EVAL_THREADS=128),
-    "e_t2k_s2_m6_t128": dict(GNA_EVAL_TILE=2048, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=6, GNA_EVAL_THREADS=128),
-    "e_t1k_s4_m7_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=4, GNA_EVAL_MINB=7, GNA_EVAL_THREADS=128),
-    "e_t1k_s2_m10_t128": dict(GNA_EVAL_TILE=1024, GNA_EVAL_STAGES=2, GNA_EVAL_MINB=10, GNA_EVAL_THREADS=128),
+    "s_a16_t256": dict(GNA_SCAN_A=16, GNA_SCAN_THREADS=256),
+    "s_a8_t256": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=256),
+    "s_a4_t256": dict(GNA_SCAN_A=4, GNA_SCAN_THREADS=256),
+    "s_a8_t128": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=128),
+    "s_a4_t128": dict(GNA_SCAN_A=4, GNA_SCAN_THREADS=128),
+    "s_a2_t128": dict(GNA_SCAN_A=2, GNA_SCAN_THREADS=128),
 }
 
 
@@ -30,7 +30,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_eval_tma.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_scan_expand.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
