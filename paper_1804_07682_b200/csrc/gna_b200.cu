@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
     for (int b = 0; b < a.nbase; ++b) {
       const double kq = phase_slope(m, a.L[b]);
       double s = 0.0;
+#pragma unroll 2
       for (int i = 0; i < a.order; ++i)
         s = fma(c_gl_w[off + i], gna::sin2c(kq, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
       // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
@@ -511,15 +512,15 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
   }
 }
 
-// stage B: block = (mass point c, chunk of kScanA (8) mixing points).  Each thread loads
+// stage B: block = (mass point c, chunk of kScanA (4) mixing points).  Each thread loads
 // G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
 // (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
 // point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
 #ifndef GNA_SCAN_A
-#define GNA_SCAN_A 8
+#define GNA_SCAN_A 4
 #endif
 #ifndef GNA_SCAN_THREADS
-#define GNA_SCAN_THREADS 256
+#define GNA_SCAN_THREADS 128
 #endif
 constexpr int kScanThreads = GNA_SCAN_THREADS;
 constexpr int kScanA = GNA_SCAN_A;
