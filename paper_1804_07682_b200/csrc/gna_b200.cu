@@ -548,9 +548,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
   const double* __restrict__ g1 = g0 + nbins;
   const double* __restrict__ g2 = g1 + nbins;
   double* __restrict__ out = spectra ? spectra + (c * nmix + a0) * nbins : nullptr;
-  for (int64_t k = threadIdx.x; k < nbins; k += kScanThreads) {
-    const double G0 = g0[k], G1 = g1[k], G2 = g2[k], H = w.H[k];
-    const double D = chi2 ? data[k] : 0.0, iD = chi2 ? w.invD[k] : 0.0;
+  // software-pipelined: the 6 loads of bin k + kScanThreads are issued before bin k's
+  // outputs are computed, so one L2 round trip is always in flight per thread
+  int64_t k = threadIdx.x;
+  double G0 = 0, G1 = 0, G2 = 0, H = 0, D = 0, iD = 0;
+  if (k < nbins) {
+    G0 = g0[k], G1 = g1[k], G2 = g2[k], H = w.H[k];
+    if (chi2) D = data[k], iD = w.invD[k];
+  }
+  for (; k < nbins; k += kScanThreads) {
+    const int64_t kn = k + kScanThreads;
+    double nG0 = 0, nG1 = 0, nG2 = 0, nH = 0, nD = 0, niD = 0;
+    if (kn < nbins) {
+      nG0 = g0[kn], nG1 = g1[kn], nG2 = g2[kn], nH = w.H[kn];
+      if (chi2) nD = data[kn], niD = w.invD[kn];
+    }
 #pragma unroll
     for (int j = 0; j < kScanA; ++j) {
       if (j < na) {
@@ -560,6 +572,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
         x2[j] = fma(d * d, iD, x2[j]);
       }
     }
+    G0 = nG0, G1 = nG1, G2 = nG2, H = nH, D = nD, iD = niD;
   }
   if (chi2) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
