@@ -109,6 +109,17 @@ int gna_oscprob_eval(const gna_osc_params* p, double L_km, const double* d_E, in
                      double* d_P, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gna_oscprob_eval_ab — NEXT-2: the general vacuum formula of P:631-639 for any
+ * channel alpha -> beta (0 = e, 1 = mu, 2 = tau):
+ *   d_P[i] = delta_ab - 4 sum_{i>j} Re(X_ij) sin^2(Delta_ij) + 2 sum_{i>j} Im(X_ij) sin(2 Delta_ij),
+ *   X_ij = V*_ai V_bi V_aj V*_bj,  V = R23 U13 R12, conj(V) for antineutrinos.
+ * Here theta23, delta_cp and the antineutrino flag matter.  Same arguments, layout
+ * and errors as gna_oscprob_eval, plus EINVAL for alpha or beta outside [0, 2].
+ * ------------------------------------------------------------------------- */
+int gna_oscprob_eval_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, double L_km,
+                        const double* d_E, int64_t n, double* d_P, void* stream);
+
+/* ---------------------------------------------------------------------------
  * gna_gl_integrate — fused P_ee + per-bin Gauss-Legendre quadrature (BJ):
  *   d_bins[k] = h_k * sum_{i<order} w_i P_ee(c_k + h_k t_i),  0 <= k < nbins.
  * d_edges: device [nbins + 1] bin edges in MeV (strictly increasing, > 0).

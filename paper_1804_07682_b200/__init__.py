@@ -25,7 +25,7 @@ __all__ = [
     "oscprob_batch_workspace_size", "oscprob_eval_host", "gl_integrate_host",
     "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
-    "oscprob_scan", "oscprob_scan_workspace_size",
+    "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab",
 ]
 
 GNA_OK, GNA_EINVAL, GNA_ECUDA, GNA_ENODEV, GNA_ENOMEM = 0, -1, -2, -3, -4
@@ -38,7 +38,7 @@ EXPORTS = (
     "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_gl_integrate_host",
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
-    "gna_oscprob_scan_workspace_size", "gna_oscprob_scan",
+    "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
 )
 
 
@@ -113,6 +113,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     B = ctypes.POINTER(_CBatch)
     L.gna_oscprob_eval.argtypes = [P, d, vp, i64, vp, vp]
     L.gna_gl_integrate.argtypes = [P, d, vp, i64, i32, vp, vp]
+    L.gna_oscprob_eval_ab.argtypes = [i32, i32, P, d, vp, i64, vp, vp]
+    L.gna_oscprob_eval_ab.restype = ctypes.c_int
     L.gna_oscprob_batch_workspace_size.argtypes = [i64, i32, i64, i32]
     L.gna_oscprob_batch_workspace_size.restype = sz
     L.gna_oscprob_batch.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
@@ -191,6 +193,21 @@ def oscprob_eval(params, L_km: float, E, out=None, stream=None):
     p = OscParams.of(params)._c()
     _check(L.gna_oscprob_eval(ctypes.byref(p), float(L_km), _dev(E, "E"), n,
                               _dev(out, "out", n), _stream(stream)), "gna_oscprob_eval")
+    return out
+
+
+def oscprob_eval_ab(alpha: int, beta: int, params, L_km: float, E, out=None, stream=None):
+    """P(nu_alpha -> nu_beta) over a device energy tensor (gna_oscprob_eval_ab, NEXT-2);
+    alpha, beta in {0: e, 1: mu, 2: tau}."""
+    import torch
+    L = load()
+    n = E.numel()
+    if out is None:
+        out = torch.empty_like(E)
+    p = OscParams.of(params)._c()
+    _check(L.gna_oscprob_eval_ab(int(alpha), int(beta), ctypes.byref(p), float(L_km),
+                                 _dev(E, "E"), n, _dev(out, "out", n), _stream(stream)),
+           "gna_oscprob_eval_ab")
     return out
 
 

@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <algorithm>
+#include <complex>
 #include <utility>
 #include <mutex>
 
@@ -77,8 +78,8 @@ __host__ __device__ inline void mixing_weights(double s12, double c12, double s1
 // ----------------------------------------------------------------------------
 
 // (a3) elementwise P_ee, double2-vectorised grid-stride stream.
-template <bool kVec>
-__global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
+template <bool kVec, class Coef>
+__global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(Coef c,
                                                                const double* __restrict__ E,
                                                                double* __restrict__ P, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -90,13 +91,13 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(PeeCoef c,
     for (int64_t i = tid; i < n2; i += stride) {
       const double2 e = __ldcs(E2 + i);
       double2 r;
-      r.x = gna::pee_inv(c, gna::rcp(e.x));
-      r.y = gna::pee_inv(c, gna::rcp(e.y));
+      r.x = gna::prob_inv(c, gna::rcp(e.x));
+      r.y = gna::prob_inv(c, gna::rcp(e.y));
       __stcs(P2 + i, r);
     }
-    if ((n & 1) && tid == 0) P[n - 1] = gna::pee_inv(c, gna::rcp(E[n - 1]));
+    if ((n & 1) && tid == 0) P[n - 1] = gna::prob_inv(c, gna::rcp(E[n - 1]));
   } else {
-    for (int64_t i = tid; i < n; i += stride) P[i] = gna::pee_inv(c, gna::rcp(E[i]));
+    for (int64_t i = tid; i < n; i += stride) P[i] = gna::prob_inv(c, gna::rcp(E[i]));
   }
 }
 
@@ -122,7 +123,8 @@ constexpr int kEvalTile = GNA_EVAL_TILE;  // doubles per tile (8 KiB)
 constexpr int kEvalStages = GNA_EVAL_STAGES;
 constexpr int kEvalTmaThreads = GNA_EVAL_THREADS;
 
-__global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval_tma(PeeCoef c,
+template <class Coef>
+__global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval_tma(Coef c,
                                                                        const double* __restrict__ E,
                                                                        double* __restrict__ P,
                                                                        int64_t n) {
@@ -152,8 +154,8 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
     for (int j = threadIdx.x; j < kEvalTile / 2; j += kEvalTmaThreads) {
       const double2 e = src[j];
       double2 r;
-      r.x = gna::pee_inv(c, gna::rcp(e.x));
-      r.y = gna::pee_inv(c, gna::rcp(e.y));
+      r.x = gna::prob_inv(c, gna::rcp(e.x));
+      r.y = gna::prob_inv(c, gna::rcp(e.y));
       __stcs(dst + j, r);
     }
     __syncthreads();  // every thread is done with stage st before it is refilled
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
   }
   if (blockIdx.x == 0)
     for (int64_t i = ntiles * kEvalTile + threadIdx.x; i < n; i += kEvalTmaThreads)
-      P[i] = gna::pee_inv(c, gna::rcp(E[i]));
+      P[i] = gna::prob_inv(c, gna::rcp(E[i]));
 }
 
 // (a3)+(a4) one parameter point.  A lane pair owns one bin: lane 2m+h evaluates the
@@ -659,6 +661,35 @@ void make_coef(const gna_osc_params* p, double L_km, PeeCoef* c) {
   c->c0 = 1.0 - 0.5 * ((w21 + w31) + w32);
 }
 
+// NEXT-2: coefficients of any channel alpha -> beta.  PMNS elements from the PDG
+// closed form (independent of the oracle's matrix product), conj for antineutrinos
+// (S:256); X_ij = V*_ai V_bi V_aj V*_bj for pairs (2,1), (3,1), (3,2).
+void make_coef_ab(int alpha, int beta, const gna_osc_params* p, double L_km, gna::PabCoef* c) {
+  using cd = std::complex<double>;
+  const double c12 = std::cos(p->theta12), s12 = std::sin(p->theta12);
+  const double c13 = std::cos(p->theta13), s13 = std::sin(p->theta13);
+  const double c23 = std::cos(p->theta23), s23 = std::sin(p->theta23);
+  const cd e = std::polar(1.0, p->delta_cp);  // e^{i delta}
+  cd V[3][3] = {{c12 * c13, s12 * c13, s13 * std::conj(e)},
+                {-s12 * c23 - c12 * s23 * s13 * e, c12 * c23 - s12 * s23 * s13 * e, s23 * c13},
+                {s12 * s23 - c12 * c23 * s13 * e, -c12 * s23 - s12 * c23 * s13 * e, c23 * c13}};
+  if (p->antineutrino)
+    for (auto& row : V)
+      for (auto& x : row) x = std::conj(x);
+  const int pi_[3] = {1, 2, 2}, pj_[3] = {0, 0, 1};
+  const double dm[3] = {p->dm2_21, p->dm2_31, p->dm2_31 - p->dm2_21};
+  double c0 = alpha == beta ? 1.0 : 0.0;
+  for (int k = 0; k < 3; ++k) {
+    const int i = pi_[k], j = pj_[k];
+    const cd X = std::conj(V[alpha][i]) * V[beta][i] * V[alpha][j] * std::conj(V[beta][j]);
+    c->kq[k] = phase_slope(dm[k], L_km);
+    c->a[k] = -4.0 * X.real();
+    c->b[k] = 2.0 * X.imag();
+    c0 += 0.5 * c->a[k];
+  }
+  c->c0 = c0;
+}
+
 int grid_for(int64_t work_items, int threads, int max_blocks) {
   int64_t b = (work_items + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -834,20 +865,21 @@ int launch_gl(const PeeCoef& c, const double* edges, int64_t nbins, int order, d
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
 
-int launch_eval(const PeeCoef& c, const double* E, int64_t n, double* P, cudaStream_t s) {
+template <class Coef>
+int launch_eval(const Coef& c, const double* E, int64_t n, double* P, cudaStream_t s) {
   const bool vec = ((((uintptr_t)E) | ((uintptr_t)P)) & 15) == 0;
   const int maxb = sm_count() * 8;
   if (vec && n >= (int64_t)kEvalTile * 4) {
     // persistent TMA-fed stream: GNA_EVAL_MINB blocks per SM (4 x 8 KiB smem ring each)
     const int64_t ntiles = n / kEvalTile;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * GNA_EVAL_MINB);
-    k_oscprob_eval_tma<<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
+    k_oscprob_eval_tma<Coef><<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
   } else if (vec) {
     const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);
-    k_oscprob_eval<true><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+    k_oscprob_eval<true, Coef><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
   } else {
     const int grid = grid_for(n, kEvalThreads, maxb);
-    k_oscprob_eval<false><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+    k_oscprob_eval<false, Coef><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -915,6 +947,18 @@ int gna_oscprob_eval(const gna_osc_params* p, double L_km, const double* d_E, in
   if (check_dev_ptr(d_E) || check_dev_ptr(d_P)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
+  return launch_eval(c, d_E, n, d_P, (cudaStream_t)stream);
+}
+
+int gna_oscprob_eval_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, double L_km,
+                        const double* d_E, int64_t n, double* d_P, void* stream) {
+  if (alpha < 0 || alpha > 2 || beta < 0 || beta > 2) return GNA_EINVAL;
+  int rc = validate_eval(p, L_km, d_E, n, d_P);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_E) || check_dev_ptr(d_P)) return GNA_EINVAL;
+  gna::PabCoef c;
+  make_coef_ab(alpha, beta, p, L_km, &c);
   return launch_eval(c, d_E, n, d_P, (cudaStream_t)stream);
 }
 

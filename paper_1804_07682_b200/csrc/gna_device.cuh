@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "sin2_poly.h"
+#include "sinpi_poly.h"
 
 namespace gna {
 
@@ -24,6 +25,10 @@ constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 // so the Horner chain needs no register or uniform-register moves.
 __constant__ double c_sin2[9] = {GNA_SIN2_C0, GNA_SIN2_C1, GNA_SIN2_C2, GNA_SIN2_C3, GNA_SIN2_C4,
                                  GNA_SIN2_C5, GNA_SIN2_C6, GNA_SIN2_C7, GNA_SIN2_C8};
+// sin(pi f) = f S(f^2), S minimax of degree 8 (sinpi_poly.h; appearance channels, NEXT-2)
+__constant__ double c_sinpi[9] = {GNA_SINPI_C0, GNA_SINPI_C1, GNA_SINPI_C2, GNA_SINPI_C3,
+                                  GNA_SINPI_C4, GNA_SINPI_C5, GNA_SINPI_C6, GNA_SINPI_C7,
+                                  GNA_SINPI_C8};
 
 // (-1)^q * V(f^2) for y = kq * invE = q + f  (y itself is never rounded separately)
 __device__ __forceinline__ double sin2c(double kq, double invE) {
@@ -54,7 +59,36 @@ __device__ __forceinline__ double rcp(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
-// Per-call coefficients of one (parameter point, baseline).
+// General term of P:633-636 for one pair: with y = kq/E = q + f,
+//   a sin^2(Delta) + b sin(2 Delta) = a/2 + (-1)^q (a v(f) + b sin(pi f)),
+// a = -4 Re X_ij, b = 2 Im X_ij.  Shares the reduction with sin2c; 24 FP64 instructions.
+__device__ __forceinline__ double sin2_sin_c(double kq, double invE, double a, double b) {
+  const double t = fma(kq, invE, kRoundMagic);
+  const double q = t - kRoundMagic;
+  const double f = fma(kq, invE, -q);
+  const double u = f * f;
+  double p = fma(u, c_sin2[8], c_sin2[7]);
+  double r = fma(u, c_sinpi[8], c_sinpi[7]);
+  p = fma(p, u, c_sin2[6]);
+  r = fma(r, u, c_sinpi[6]);
+  p = fma(p, u, c_sin2[5]);
+  r = fma(r, u, c_sinpi[5]);
+  p = fma(p, u, c_sin2[4]);
+  r = fma(r, u, c_sinpi[4]);
+  p = fma(p, u, c_sin2[3]);
+  r = fma(r, u, c_sinpi[3]);
+  p = fma(p, u, c_sin2[2]);
+  r = fma(r, u, c_sinpi[2]);
+  p = fma(p, u, c_sin2[1]);
+  r = fma(r, u, c_sinpi[1]);
+  p = fma(p, u, c_sin2[0]);
+  r = fma(r, u, c_sinpi[0]);
+  const double g = fma(b * f, r, a * p);
+  const int odd = __double2loint(t) << 31;
+  return __hiloint2double(__double2hiint(g) ^ odd, __double2loint(g));
+}
+
+// Per-call coefficients of one (parameter point, baseline): P_ee (the hot path).
 struct PeeCoef {
   double kq[3];  // phase slopes in units of pi/2 per (1/MeV): y_ij = kq_ij / E
   double w[3];   // mixing weights w21, w31, w32 (optionally times a baseline weight)
@@ -67,5 +101,24 @@ __device__ __forceinline__ double pee_inv(const PeeCoef& c, double invE) {
   acc = fma(c.w[2], sin2c(c.kq[2], invE), acc);
   return c.c0 - acc;
 }
+
+// Any channel alpha -> beta (NEXT-2): P = c0 + sum_ij (-1)^q (a_ij v + b_ij sin(pi f)),
+// c0 = delta_ab + sum_ij a_ij / 2.
+struct PabCoef {
+  double kq[3];
+  double a[3];  // -4 Re X_ij
+  double b[3];  //  2 Im X_ij
+  double c0;
+};
+
+__device__ __forceinline__ double pab_inv(const PabCoef& c, double invE) {
+  double acc = sin2_sin_c(c.kq[0], invE, c.a[0], c.b[0]);
+  acc += sin2_sin_c(c.kq[1], invE, c.a[1], c.b[1]);
+  acc += sin2_sin_c(c.kq[2], invE, c.a[2], c.b[2]);
+  return c.c0 + acc;
+}
+
+__device__ __forceinline__ double prob_inv(const PeeCoef& c, double invE) { return pee_inv(c, invE); }
+__device__ __forceinline__ double prob_inv(const PabCoef& c, double invE) { return pab_inv(c, invE); }
 
 }  // namespace gna

@@ -89,6 +89,15 @@ def test_eval_einval(lib, case):
         assert f() == gna.GNA_EINVAL
 
 
+@pytest.mark.parametrize("ab", [(-1, 0), (0, 3), (3, 3), (0, -2)])
+def test_eval_ab_einval(lib, ab):
+    assert lib.gna_oscprob_eval_ab(ab[0], ab[1], _params(), 52.5, BAD, 10, BAD2, None) == \
+        gna.GNA_EINVAL
+    # and the shared validation
+    assert lib.gna_oscprob_eval_ab(0, 1, _params(), -1.0, BAD, 10, BAD2, None) == gna.GNA_EINVAL
+    assert lib.gna_oscprob_eval_ab(0, 1, _params(), 1.0, BAD, 0, BAD2, None) == gna.GNA_EINVAL
+
+
 def test_eval_null_params(lib):
     assert lib.gna_oscprob_eval(None, 1.0, BAD, 10, BAD2, None) == gna.GNA_EINVAL
 
@@ -211,6 +220,31 @@ def _sin2_coeffs():
     src = open(os.path.join(_build.CSRC, "sin2_poly.h")).read()
     cs = dict(re.findall(r"#define GNA_SIN2_C(\d) \(([-0-9a-fx.p+]+)\)", src))
     return [float.fromhex(cs[str(j)]) for j in range(len(cs))]
+
+
+def _sinpi_coeffs():
+    src = open(os.path.join(_build.CSRC, "sinpi_poly.h")).read()
+    cs = dict(re.findall(r"#define GNA_SINPI_C(\d) \(([-0-9a-fx.p+]+)\)", src))
+    return [float.fromhex(cs[str(j)]) for j in range(len(cs))]
+
+
+def test_kernel_sinpi_polynomial_accuracy():
+    """sin(pi (q + f)) = (-1)^q f S(f^2) with the kernel's fp64 Horner: |err| <= 2.5e-16."""
+    cf = _sinpi_coeffs()
+    assert len(cf) == 9
+    mp.mp.dps = 40
+    fs = np.r_[np.linspace(-0.5, 0.5, 801), np.random.default_rng(4).uniform(-0.5, 0.5, 400)]
+    worst = 0.0
+    for f in fs:
+        u = float(f) * float(f)
+        p = cf[-1]
+        for c in reversed(cf[:-1]):
+            p = _fma(p, u, c)
+        got = float(f) * p
+        for q in (0, 3):
+            ref = mp.sin(mp.pi * (q + mp.mpf(float(f))))
+            worst = max(worst, abs((got if q % 2 == 0 else -got) - float(ref)))
+    assert worst <= 2.5e-16
 
 
 def _fma(a, b, c):

@@ -135,6 +135,49 @@ def test_eval_cfg3_full_size_sampled(gna):
     torch.cuda.empty_cache()
 
 
+# ------------------------------------------------------------------------ NEXT-2 any channel
+@pytest.mark.parametrize("n", [5, 4097, 100_003])
+def test_eval_ab_all_channels_vs_oracle(gna, n):
+    g = synth.rng(600 + n)
+    for _ in range(3):
+        p = synth.random_params(g)  # random theta23, delta, nu/nubar: they matter here
+        L = g.uniform(0, 300)
+        E = synth.random_energies(g, n)
+        Et = _t(E)
+        rows = []
+        for a in range(3):
+            row = []
+            for b in range(3):
+                P = _np(gna.oscprob_eval_ab(a, b, p, L, Et))
+                Pr = oracle.prob_array(p, L, E, alpha=a, beta=b, nthreads=_nt())
+                assert np.max(np.abs(P - Pr)) <= TOL_P, (a, b, p, L)
+                row.append(P)
+            rows.append(row)
+        M = np.array(rows)  # [alpha][beta][n]
+        assert np.max(np.abs(M.sum(axis=1) - 1)) <= 4 * TOL_P  # unitarity
+        assert np.max(np.abs(M.sum(axis=0) - 1)) <= 4 * TOL_P
+        # the e->e channel of the general path agrees with the P_ee hot path
+        Pee = _np(gna.oscprob_eval(p, L, Et))
+        assert np.max(np.abs(M[0, 0] - Pee)) <= 1e-14
+
+
+def test_eval_ab_cpt_and_L0(gna):
+    g = synth.rng(61)
+    p = synth.random_params(g)
+    p["antineutrino"] = 0
+    E = synth.random_energies(g, 5000)
+    Et = _t(E)
+    pm = dict(p, delta_cp=-p["delta_cp"])
+    for a in range(3):
+        for b in range(3):
+            # CPT: P_ab(delta) = P_ba(-delta)
+            assert np.max(np.abs(_np(gna.oscprob_eval_ab(a, b, p, 80.0, Et))
+                                 - _np(gna.oscprob_eval_ab(b, a, pm, 80.0, Et)))) <= 2 * TOL_P
+            # L = 0 -> delta_ab
+            P0 = _np(gna.oscprob_eval_ab(a, b, p, 0.0, Et))
+            assert np.max(np.abs(P0 - (1.0 if a == b else 0.0))) <= 4 * EPS
+
+
 # ------------------------------------------------------------------------ (a4) GL
 def test_gl_cfg1(gna):
     c = synth.config("cfg1")
