@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "cfg2", "cfg1",
-                                                            "cfg4grid"])
+                                                            "cfg4grid", "cfg3emu"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunks", type=int, default=0, help="gather pipeline chunks (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -67,7 +67,9 @@ def parse():
 
 # ----------------------------------------------------------------------------- workloads
 def workload(name: str) -> dict:
-    c = synth.config(name)
+    c = synth.config("cfg3" if name == "cfg3emu" else name)
+    if name == "cfg3emu":
+        c["params"] = dict(c["params"], delta_cp=1.2)
     if name in ("cfg4", "cfg5"):
         P = c["points"]["theta12"].size
         nb = c["edges"].size - 1
@@ -77,6 +79,12 @@ def workload(name: str) -> dict:
                          "(%d bins x GL%d), spectra + chi2 per point" % (
                              name, c["L_km"].size, P, nb * c["order"], nb, c["order"]),
                          points=P, baselines=int(c["L_km"].size), bins=nb, order=c["order"])
+    elif name == "cfg3emu":
+        c["evals"] = c["n"]
+        c["bins_total"] = 0
+        c["desc"] = dict(workload="cfg3emu: NEXT-2 appearance channel nu_e -> nu_mu (general "
+                         "formula P:633-636, delta_cp = 1.2, theta23 = 0.785) over %d energies "
+                         "streamed from HBM" % c["n"], points=1, energies=c["n"])
     elif name == "cfg4grid":
         nmix, nmass = c["grid"]["theta12"].size, c["grid"]["dm2_21"].size
         nb = c["edges"].size - 1
@@ -216,7 +224,8 @@ def run_reference(args, rank, world):
             u = c["evals"]
         else:
             E = np.linspace(c["lo"], c["hi"], ns)
-            oracle.prob_array(c["params"], c["L_km"], E, nthreads=nt)
+            ab = (0, 1) if args.workload == "cfg3emu" else (0, 0)
+            oracle.prob_array(c["params"], c["L_km"], E, alpha=ab[0], beta=ab[1], nthreads=nt)
             u = ns
         return time.perf_counter() - t0, u
 
@@ -226,7 +235,7 @@ def run_reference(args, rank, world):
     rate = u / max(dt, 1e-9)
     per_step = max(0.05, min(args.cpu_seconds, 120.0) / max(args.steps + args.warmup, 1))
     full = {"cfg4": 10_000, "cfg5": 1000, "cfg2": 100_000, "cfg3": 100_000_000,
-            "cfg1": 100, "cfg4grid": 10_000}[args.workload]
+            "cfg1": 100, "cfg4grid": 10_000, "cfg3emu": 100_000_000}[args.workload]
     unit_per = u / ns
     ns = int(max(1, min(full, rate * per_step / unit_per)))
     for _ in range(args.warmup):
@@ -290,8 +299,9 @@ def cpu_baseline(c, name, seconds):
     else:
         n = 20_000_000
         E = np.linspace(c["lo"], c["hi"], n)
+        ab = (0, 1) if name == "cfg3emu" else (0, 0)
         t0 = time.perf_counter()
-        oracle.prob_array(c["params"], c["L_km"], E, nthreads=nt)
+        oracle.prob_array(c["params"], c["L_km"], E, alpha=ab[0], beta=ab[1], nthreads=nt)
         dt = time.perf_counter() - t0
         units = n
         sample = "%d of %d energies of cfg3 (same linspace range)" % (n, c["n"])
@@ -404,6 +414,18 @@ def main():
         units_per_rank = c["evals"]
         calls_per_step = 1
         scaling = "weak"  # replicas only
+    elif args.workload == "cfg3emu":
+        E = torch.linspace(c["lo"], c["hi"], c["n"], **f64)
+        out = torch.empty_like(E)
+        kern_ev = []
+
+        def step():
+            with KernelTimer(kern_ev):
+                gna.oscprob_eval_ab(0, 1, c["params"], c["L_km"], E, out=out)
+
+        units_per_rank = c["evals"]
+        calls_per_step = 1
+        scaling = "weak"  # replicas only
     else:
         E = torch.linspace(c["lo"], c["hi"], c["n"], **f64)
         out = torch.empty_like(E)
@@ -497,6 +519,15 @@ def main():
                 "peak_source": peaks["source"],
                 "note": "whole gna_oscprob_scan call (stage-A sin^2 tables + rank-3 expansion "
                         "+ chi2 reduce); algorithmic bytes = spectra written"}
+    elif args.workload == "cfg3emu":
+        # general channel: 3 pairs x 24 FP64 + reciprocal 6 + 1 = 79 FP64 slots per energy
+        ops = 3 * 24 + 6 + 1
+        achieved = units_per_rank * ops / (kern_avg_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
+                "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
+                "ops_per_energy_point": ops,
+                "hbm_frac": units_per_rank * 16 / (kern_avg_ms * 1e-3) / 1e9 /
+                _measured_peaks()["hbm_gbs"]}
     elif args.workload == "cfg3":
         # co-limited stream: report the HBM side (16 B per energy) and note FP64
         launch_units = units_per_rank
@@ -536,11 +567,11 @@ def main():
             "cuda_graph": bool(use_graph)}
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
-    if not args.no_e2e and args.workload != "cfg4grid":
+    if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu"):
         line["e2e"] = e2e(args, c, gna, torch, dist, dev, world, rank, local)
-    elif args.workload == "cfg4grid":
+    elif args.workload in ("cfg4grid", "cfg3emu"):
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0, "note": "no host-buffer variant of the scan yet"}
+                       "d2h_bytes_per_step": 0, "note": "no host-buffer variant for this NEXT row yet"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c, args.workload, args.cpu_seconds)
