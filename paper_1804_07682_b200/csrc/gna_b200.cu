@@ -307,6 +307,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 #define GNA_PRAGMA(x) _Pragma(#x)
 #define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
+#ifndef GNA_BATCH_LDS_PREFETCH
+#define GNA_BATCH_LDS_PREFETCH 0
+#endif
 #ifndef GNA_BATCH_JUNROLL
 #define GNA_BATCH_JUNROLL 1
 #endif
@@ -327,12 +330,25 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     iE[n] = invE[(int64_t)(i + n) * nbins];
     a[n] = 0.0;
   }
+#if GNA_BATCH_LDS_PREFETCH
+  // the next coefficient pair is loaded before the current one is consumed, so the
+  // LDS latency is not exposed at the top of every iteration
+  double2 cw = sc[0];
+  GNA_UNROLL(GNA_BATCH_JUNROLL)
+  for (int j = 0; j < nterm; ++j) {
+    const double2 cn = sc[j + 1 < nterm ? j + 1 : j];
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+    cw = cn;
+  }
+#else
   GNA_UNROLL(GNA_BATCH_JUNROLL)
   for (int j = 0; j < nterm; ++j) {
     const double2 cw = sc[j];
 #pragma unroll
     for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
   }
+#endif
 #pragma unroll
   for (int n = 0; n < N; ++n) s = fma(hw[(int64_t)(i + n) * nbins], c0 - a[n], s);
 }

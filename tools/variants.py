@@ -12,12 +12,11 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "s_a16_t256": dict(GNA_SCAN_A=16, GNA_SCAN_THREADS=256),
-    "s_a8_t256": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=256),
-    "s_a4_t256": dict(GNA_SCAN_A=4, GNA_SCAN_THREADS=256),
-    "s_a8_t128": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=128),
-    "s_a4_t128": dict(GNA_SCAN_A=4, GNA_SCAN_THREADS=128),
-    "s_a2_t128": dict(GNA_SCAN_A=2, GNA_SCAN_THREADS=128),
+    "b_base": dict(),
+    "b_pf": dict(GNA_BATCH_LDS_PREFETCH=1),
+    "b_u2": dict(GNA_BATCH_JUNROLL=2),
+    "b_pf_u2": dict(GNA_BATCH_LDS_PREFETCH=1, GNA_BATCH_JUNROLL=2),
+    "b_pf_m5": dict(GNA_BATCH_LDS_PREFETCH=1, GNA_BATCH_MINB=20),
 }
 
 
@@ -30,7 +29,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_scan_expand.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_batchILi1ELi5E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
