@@ -307,6 +307,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 #define GNA_PRAGMA(x) _Pragma(#x)
 #define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
+#ifndef GNA_BATCH_SMALL_NBASE
+#define GNA_BATCH_SMALL_NBASE 0
+#endif
 #ifndef GNA_BATCH_LDS_PREFETCH
 #define GNA_BATCH_LDS_PREFETCH 0
 #endif
@@ -814,8 +817,10 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
 
   const int nterm = 3 * nbase;
   const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
-  // node-group size: 5, 4 or 3 when it divides the order, else 4
-  auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5>
+  // node-group size: 5, 4 or 3 when it divides the order, else 4; with few terms per
+  // node (nbase <= GNA_BATCH_SMALL_NBASE) a 10-node group (GL10) amortises the group overhead
+  auto kern = (order == 10 && nbase <= GNA_BATCH_SMALL_NBASE) ? k_oscprob_batch<kBatchWarps, 10>
+              : (order % 5 == 0)                             ? k_oscprob_batch<kBatchWarps, 5>
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4>
               : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3>
                                  : k_oscprob_batch<kBatchWarps, 4>;

@@ -13,10 +13,8 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "b_base": dict(),
-    "b_pf": dict(GNA_BATCH_LDS_PREFETCH=1),
-    "b_u2": dict(GNA_BATCH_JUNROLL=2),
-    "b_pf_u2": dict(GNA_BATCH_LDS_PREFETCH=1, GNA_BATCH_JUNROLL=2),
-    "b_pf_m5": dict(GNA_BATCH_LDS_PREFETCH=1, GNA_BATCH_MINB=20),
+    "b_small1": dict(GNA_BATCH_SMALL_NBASE=1),
+    "b_small8": dict(GNA_BATCH_SMALL_NBASE=8),
 }
 
 
@@ -29,7 +27,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_batchILi1ELi5E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_batchILi1ELi10E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
