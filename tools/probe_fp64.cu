@@ -5,6 +5,7 @@
 // no FP64 number). Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 probe_fp64.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
@@ -98,6 +99,43 @@ __global__ void k_dfma_int(double* out, double a, double b, int iters) {
   if (s == 12345.678 || t == 0x12345u) out[0] = s + t;
 }
 
+// F2F.F32.F64 (double -> float, round to nearest) alternating with a DADD: rate of the
+// conversion relative to the FP64 pipe (mixed-precision tier, NEXT-3)
+__global__ void k_f2f(double* out, double a, double b, int iters) {
+  double x[CH];
+  float y[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) { x[c] = 1.5 + threadIdx.x * 1e-3 + c; y[c] = 0.f; }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const float f = __double2float_rn(x[c]);
+      y[c] = fmaf(y[c], 0.999f, f);
+      x[c] = x[c] + a;
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c] + y[c];
+  if (s == 12345.678) out[0] = s;
+}
+
+// FP32 FFMA chains (FP32 pipe rate)
+__global__ void k_ffma(double* out, double a, double b, int iters) {
+  float x[CH];
+  const float fa = (float)a, fb = (float)b;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) x[c] = threadIdx.x * 1e-3f + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) x[c] = fmaf(x[c], fa, fb);
+  }
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) s += x[c];
+  if (s == 12345.678f) out[0] = s;
+}
+
 typedef void (*kfn)(double*, double, double, int);
 
 static int run(const char* name, kfn f, double ops_per_inner, int blocks, int threads, int iters,
@@ -133,8 +171,9 @@ int main() {
     run("frnd+dadd(count=pairs)", k_frnd, 1.0, sms * occ, 256, 10000, d_out);
     run("rcp64h+dadd(count=pairs)", k_rcp, 1.0, sms * occ, 256, 10000, d_out);
     run("dfma+int(count=dfma)", k_dfma_int, 1.0, sms * occ, 256, 20000, d_out);
+    run("f2f+ffma+dadd(count=triples)", k_f2f, 1.0, sms * occ, 256, 10000, d_out);
+    run("ffma", k_ffma, 1.0, sms * occ, 256, 40000, d_out);
   }
-  // long run for clocks under sustained FP64 load (~3 s)
-  run("dfma_sustained", k_dfma, 1.0, sms * 8, 256, 800000, d_out);
+  if (getenv("PROBE_SUSTAINED")) run("dfma_sustained", k_dfma, 1.0, sms * 8, 256, 800000, d_out);
   return 0;
 }
