@@ -178,6 +178,42 @@ def test_eval_ab_cpt_and_L0(gna):
             assert np.max(np.abs(P0 - (1.0 if a == b else 0.0))) <= 4 * EPS
 
 
+# ------------------------------------------------------------------------ 64-bit indexing
+def test_eval_beyond_int32_elements(gna):
+    """n = 2^31 + 123 energies (17 GB in, 17 GB out on the 180 GB B200): 64-bit tile and tail indexing."""
+    import torch
+    n = (1 << 31) + 123
+    E = torch.linspace(1.0, 10.0, n, dtype=torch.float64, device="cuda")
+    P = gna.oscprob_eval(synth.CANONICAL, 52.5, E)
+    idx = np.r_[0:8, (1 << 31) - 4:(1 << 31) + 4, n - 130:n, synth.rng(8).integers(0, n, 2000)]
+    it = torch.tensor(idx, device="cuda")
+    Es, Ps = _np(E[it]), _np(P[it])
+    assert np.max(np.abs(Ps - oracle.prob_array(synth.CANONICAL, 52.5, Es))) <= TOL_P
+    del E, P, it
+    torch.cuda.empty_cache()
+
+
+def test_batch_spectra_beyond_int32_elements(gna):
+    """P x nbins = 2.2e9 > 2^31 spectra elements (17.6 GB): 64-bit output indexing."""
+    import torch
+    P, nbins = 220_000, 10_000
+    g = synth.rng(31)
+    pts = synth.points_uniform(g, P, dict(theta13=(0.1, 0.2), dm2_31=(2.3e-3, 2.7e-3)))
+    edges = synth.uniform_edges(nbins)
+    data = synth.pseudo_data(g, edges, 1.0)
+    sp, x2 = gna.oscprob_batch({k: _t(v) for k, v in pts.items()}, [52.5], [1.0], _t(edges), 1,
+                               data=_t(data))
+    rows = np.array([0, 1, 214_748, 214_749, P - 1])  # rows around p * nbins = 2^31
+    sps = _np(sp[torch.tensor(rows, device="cuda")])
+    x2s = _np(x2)[rows]
+    spr, x2r = oracle.batch(synth.subset_points(pts, rows), [52.5], [1.0], edges, 1, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sps - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2s - x2r) <= _chi2_bound(spr, data))
+    del sp, x2
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------------------ (a4) GL
 def test_gl_cfg1(gna):
     c = synth.config("cfg1")
