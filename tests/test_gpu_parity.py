@@ -409,6 +409,67 @@ def test_batch_host_bitwise_equals_device(gna):
     assert np.array_equal(x2h2, x2d)
 
 
+# ------------------------------------------------------------------------ streams and graphs
+def test_batch_capturable_in_cuda_graph(gna):
+    """The device entry points are stream-ordered and allocation-free: they can be captured
+    in a CUDA graph and replayed (bench.py does this); replay == eager, bitwise."""
+    import torch
+    g = synth.rng(71)
+    pts, L, om, edges, data = _batch_case(g, 9, 4, 300, 10)
+    dp = {k: _t(v) for k, v in pts.items()}
+    de, dd = _t(edges), _t(data)
+    sp = torch.empty((9, 300), dtype=torch.float64, device="cuda")
+    x2 = torch.empty(9, dtype=torch.float64, device="cuda")
+    ws = torch.empty(gna.oscprob_batch_workspace_size(9, 4, 300, 10) // 8 + 2,
+                     dtype=torch.float64, device="cuda")
+    gna.oscprob_batch(dp, L, om, de, 10, data=dd, spectra=sp, chi2=x2, workspace=ws)
+    ref_sp, ref_x2 = _np(sp).copy(), _np(x2).copy()
+    sp.zero_()
+    x2.zero_()
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            gna.oscprob_batch(dp, L, om, de, 10, data=dd, spectra=sp, chi2=x2, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        graph.replay()
+    assert np.array_equal(_np(sp), ref_sp) and np.array_equal(_np(x2), ref_x2)
+
+
+def test_concurrent_calls_on_two_streams(gna):
+    """Concurrent calls on disjoint outputs on two non-default streams."""
+    import torch
+    g = synth.rng(72)
+    p1, p2 = synth.random_params(g), synth.random_params(g)
+    E = _t(synth.random_energies(g, 300_000))
+    edges = _t(np.sort(g.uniform(1, 10, 20_001)))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        a = gna.oscprob_eval(p1, 100.0, E)
+        b = gna.gl_integrate(p1, 100.0, edges, 7)
+    with torch.cuda.stream(s2):
+        c = gna.oscprob_eval(p2, 30.0, E)
+        d = gna.gl_integrate(p2, 30.0, edges, 9)
+    torch.cuda.synchronize()
+    assert np.array_equal(_np(a), _np(gna.oscprob_eval(p1, 100.0, E)))
+    assert np.array_equal(_np(b), _np(gna.gl_integrate(p1, 100.0, edges, 7)))
+    assert np.array_equal(_np(c), _np(gna.oscprob_eval(p2, 30.0, E)))
+    assert np.array_equal(_np(d), _np(gna.gl_integrate(p2, 30.0, edges, 9)))
+
+
+def test_repeated_calls_bitwise_deterministic(gna):
+    g = synth.rng(73)
+    p = synth.random_params(g)
+    E = _t(synth.random_energies(g, 1_000_003))
+    r0 = _np(gna.oscprob_eval(p, 52.5, E)).copy()
+    for _ in range(3):
+        assert np.array_equal(_np(gna.oscprob_eval(p, 52.5, E)), r0)
+
+
 # ------------------------------------------------------------------------ ABI on the GPU
 def test_host_pointer_to_device_entry_is_einval(gna):
     import ctypes
