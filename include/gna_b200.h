@@ -156,6 +156,32 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
                       void* d_workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gna_oscprob_batch_ex — gna_oscprob_batch with the gather fused into the kernel
+ * epilogue: d_spectra / d_chi2 may point into another GPU's
+ * memory (a symmetric-memory window over NVLink) instead of this GPU's, so that
+ * each rank writes its rows of the gathered result directly, with no separate
+ * collective.
+ *   flags = 0                  same as gna_oscprob_batch;
+ *   flags = GNA_OUT_PEER       outputs are peer-mapped unicast addresses (e.g. the
+ *                              root's buffer): plain stores + a system-scope fence;
+ *   flags = GNA_OUT_MULTICAST  outputs are NVLS multicast addresses: multimem.st
+ *                              writes every participating GPU's copy (all-gather).
+ * The caller synchronises the ranks after the call (e.g. a symmetric-memory or
+ * NCCL barrier on the stream) before reading the gathered result.  Inputs and the
+ * workspace must be this GPU's memory; output pointers are not type-checked.
+ * Other arguments and errors as gna_oscprob_batch; EINVAL for unknown or
+ * conflicting flags.
+ * ------------------------------------------------------------------------- */
+#define GNA_OUT_PEER 1u
+#define GNA_OUT_MULTICAST 2u
+
+int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const double* omega,
+                         int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                         double* d_spectra, const double* d_data, double* d_chi2,
+                         void* d_workspace, size_t workspace_bytes, uint32_t flags,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
  * gna_oscprob_scan — separable grid scan (the paper's
  * "computed only once ... re-computed only if any of the variables or inputs it
  * depends on were modified", and one transformation per formula item,

@@ -25,7 +25,8 @@ __all__ = [
     "oscprob_batch_workspace_size", "oscprob_eval_host", "gl_integrate_host",
     "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
-    "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab",
+    "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab", "oscprob_batch_ex",
+    "GNA_OUT_PEER", "GNA_OUT_MULTICAST",
 ]
 
 GNA_OK, GNA_EINVAL, GNA_ECUDA, GNA_ENODEV, GNA_ENOMEM = 0, -1, -2, -3, -4
@@ -39,7 +40,11 @@ EXPORTS = (
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
     "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
+    "gna_oscprob_batch_ex",
 )
+
+GNA_OUT_PEER = 1
+GNA_OUT_MULTICAST = 2
 
 
 class GnaError(RuntimeError):
@@ -114,6 +119,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_oscprob_eval.argtypes = [P, d, vp, i64, vp, vp]
     L.gna_gl_integrate.argtypes = [P, d, vp, i64, i32, vp, vp]
     L.gna_oscprob_eval_ab.argtypes = [i32, i32, P, d, vp, i64, vp, vp]
+    L.gna_oscprob_batch_ex.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz,
+                                       ctypes.c_uint32, vp]
+    L.gna_oscprob_batch_ex.restype = ctypes.c_int
     L.gna_oscprob_eval_ab.restype = ctypes.c_int
     L.gna_oscprob_batch_workspace_size.argtypes = [i64, i32, i64, i32]
     L.gna_oscprob_batch_workspace_size.restype = sz
@@ -307,6 +315,26 @@ def oscprob_scan(grid: dict, L_km, omega, edges, order: int, data=None, spectra=
         _dev(chi2, "chi2", nmass * nmix) if chi2 is not None else None,
         workspace.data_ptr(), workspace.numel() * 8, _stream(stream)), "gna_oscprob_scan")
     return spectra, chi2
+
+
+def oscprob_batch_ex(points: dict, L_km, omega, edges, order: int, spectra_ptr: int | None,
+                     chi2_ptr: int | None, flags: int, data=None, workspace=None, stream=None):
+    """gna_oscprob_batch_ex (NEXT-4): outputs are raw addresses of a remote window (peer or
+    NVLS multicast VA from symmetric memory, see dist.FusedGather); inputs are local tensors."""
+    import torch
+    L = load()
+    P = points["theta12"].numel()
+    nbins = edges.numel() - 1
+    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    if workspace is None:
+        wb = oscprob_batch_workspace_size(P, Lh.size, nbins, order)
+        workspace = torch.empty(max(wb // 8, 2), dtype=torch.float64, device=edges.device)
+    b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
+    _check(L.gna_oscprob_batch_ex(
+        ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins,
+        int(order), spectra_ptr, _dev(data, "data", nbins) if data is not None else None,
+        chi2_ptr, _dev(workspace, "workspace"), workspace.numel() * 8, int(flags),
+        _stream(stream)), "gna_oscprob_batch_ex")
 
 
 # ---------------------------------------------------------------- host-buffer entry points

@@ -307,9 +307,6 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 #define GNA_PRAGMA(x) _Pragma(#x)
 #define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
-#ifndef GNA_BATCH_SMALL_NBASE
-#define GNA_BATCH_SMALL_NBASE 0
-#endif
 #ifndef GNA_BATCH_LDS_PREFETCH
 #define GNA_BATCH_LDS_PREFETCH 0
 #endif
@@ -371,11 +368,27 @@ __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc
   }
 }
 
+// Output stores of the batch epilogue (NEXT-4, fused gather):
+//   kOutLocal     plain stores to this GPU's memory;
+//   kOutPeer      plain stores to a peer GPU's memory mapped into this address space
+//                 (symmetric memory over NVLink), system-scope fence at the end;
+//   kOutMulticast multimem.st to an NVLink-SHARP (NVLS) multicast address: one store
+//                 lands in every participating GPU's buffer (all-gather in the epilogue).
+enum { kOutLocal = 0, kOutPeer = 1, kOutMulticast = 2 };
+
+template <int kOut>
+__device__ __forceinline__ void out_store(double* p, double v) {
+  if constexpr (kOut == kOutMulticast)
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  else
+    *p = v;
+}
+
 // (a3)+(a4)+(a5) main pass.  Block = (point p, kWarps x 32 bins); every warp is
 // independent (no block barrier): it copies its point's coefficient row into a
 // warp-private smem slice, then each lane integrates one bin, N GL nodes at a time
 // (N divides the order when possible, so no group runs with reduced ILP).
-template <int kWarps, int N>
+template <int kWarps, int N, int kOut>
 __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
     double x2 = 0.0;
     if (active) {
-      if (spectra) spectra[p * nbins + k] = s;
+      if (spectra) out_store<kOut>(spectra + p * nbins + k, s);
       const double d = s - D;
       x2 = d * d / D;
     }
@@ -417,10 +430,12 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
       if (lane == 0) w.partial[p * wpp + wt] = x2;
     }
   }
+  if constexpr (kOut != kOutLocal) __threadfence_system();  // remote stores before completion
 }
 
 // chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
 // in order, then a fixed xor tree (deterministic, independent of scheduling).
+template <int kOut>
 __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
                                                                 int64_t npoints, int64_t wpp,
                                                                 double* __restrict__ chi2) {
@@ -432,7 +447,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __
   for (int64_t j = lane; j < wpp; j += 32) s += q[j];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) chi2[p] = s;
+  if (lane == 0) out_store<kOut>(chi2 + p, s);
+  if constexpr (kOut != kOutLocal) __threadfence_system();
 }
 
 // ----------------------------------------------------------------------------
@@ -779,10 +795,11 @@ int64_t blocks_per_point(int64_t nbins) {
 }
 
 // launch of the batch kernels on already-validated device arguments
-int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
-                 int32_t nbase, const double* edges, int64_t nbins, int32_t order,
-                 double* spectra, const double* data, double* chi2, void* workspace,
-                 cudaStream_t s) {
+template <int kOut>
+int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double* omega,
+                   int32_t nbase, const double* edges, int64_t nbins, int32_t order,
+                   double* spectra, const double* data, double* chi2, void* workspace,
+                   cudaStream_t s) {
   BatchSetupArgs a;
   std::memset(&a, 0, sizeof(a));
   double om = 0.0;
@@ -817,13 +834,11 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
 
   const int nterm = 3 * nbase;
   const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
-  // node-group size: 5, 4 or 3 when it divides the order, else 4; with few terms per
-  // node (nbase <= GNA_BATCH_SMALL_NBASE) a 10-node group (GL10) amortises the group overhead
-  auto kern = (order == 10 && nbase <= GNA_BATCH_SMALL_NBASE) ? k_oscprob_batch<kBatchWarps, 10>
-              : (order % 5 == 0)                             ? k_oscprob_batch<kBatchWarps, 5>
-              : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4>
-              : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3>
-                                 : k_oscprob_batch<kBatchWarps, 4>;
+  // node-group size: 5, 4 or 3 when it divides the order, else 4
+  auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5, kOut>
+              : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut>
+              : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut>
+                                 : k_oscprob_batch<kBatchWarps, 4, kOut>;
   kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
       nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -832,13 +847,27 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
   if (chi2) {
     const int64_t threads = pts->npoints * 32;
     const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
-    k_chi2_reduce<<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints, warps_per_point(nbins),
-                                                  chi2);
+    k_chi2_reduce<kOut><<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints,
+                                                        warps_per_point(nbins), chi2);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);
   }
   return GNA_OK;
+}
+
+int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                 int32_t nbase, const double* edges, int64_t nbins, int32_t order,
+                 double* spectra, const double* data, double* chi2, void* workspace,
+                 cudaStream_t s, int out_mode = kOutLocal) {
+  if (out_mode == kOutMulticast)
+    return launch_batch_k<kOutMulticast>(pts, L_km, omega, nbase, edges, nbins, order, spectra,
+                                         data, chi2, workspace, s);
+  if (out_mode == kOutPeer)
+    return launch_batch_k<kOutPeer>(pts, L_km, omega, nbase, edges, nbins, order, spectra, data,
+                                    chi2, workspace, s);
+  return launch_batch_k<kOutLocal>(pts, L_km, omega, nbase, edges, nbins, order, spectra, data,
+                                   chi2, workspace, s);
 }
 
 int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega, int32_t nbase,
@@ -1106,6 +1135,35 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_scan(g, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
                      d_workspace, (cudaStream_t)stream);
+}
+
+int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const double* omega,
+                         int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                         double* d_spectra, const double* d_data, double* d_chi2,
+                         void* d_workspace, size_t workspace_bytes, uint32_t flags,
+                         void* stream) {
+  const uint32_t known = GNA_OUT_PEER | GNA_OUT_MULTICAST;
+  if ((flags & ~known) || ((flags & GNA_OUT_PEER) && (flags & GNA_OUT_MULTICAST)))
+    return GNA_EINVAL;
+  if (flags == 0)
+    return gna_oscprob_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
+                             d_chi2, d_workspace, workspace_bytes, stream);
+  int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
+                          d_chi2);
+  if (rc) return rc;
+  if (!d_workspace ||
+      workspace_bytes < batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr) ||
+      ((uintptr_t)d_workspace & 15))
+    return GNA_EINVAL;
+  if ((rc = check_device())) return rc;
+  // inputs and workspace must be this GPU's memory; the outputs are remote windows
+  const void* ptrs[7] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, d_edges, d_data,
+                         d_workspace};
+  for (const void* q : ptrs)
+    if (q && check_dev_ptr(q)) return GNA_EINVAL;
+  return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
+                      d_workspace, (cudaStream_t)stream,
+                      (flags & GNA_OUT_MULTICAST) ? kOutMulticast : kOutPeer);
 }
 
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,

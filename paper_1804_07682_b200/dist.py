@@ -151,3 +151,59 @@ class ShardedBatch:
             flat = torch.cat([g.reshape(-1) for g in self.g_chi2])
             x = flat.index_select(0, pos)
         return s, x
+
+
+class FusedGather:
+    """NEXT-4: the gather fused into the batch kernel's epilogue over NVLink.
+
+    The gathered spectra [P, nbins] and chi2 [P] live in symmetric memory
+    (torch.distributed._symmetric_memory: every rank's buffer is mapped into every
+    rank's address space).  Rank r's kernel writes its rows [lo_r, hi_r) directly:
+      * multicast (NVLS, when the fabric supports it): multimem stores to the
+        multicast address, so every rank ends with the full result (all-gather);
+      * otherwise: plain stores into rank 0's buffer over NVLink (gather to root).
+    A symmetric-memory barrier on the stream then orders the remote writes before any
+    rank reads.  No separate collective moves the data.
+    """
+
+    def __init__(self, npoints: int, nbins: int, device, group=None, prefer_multicast=True):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.npoints, self.nbins = npoints, nbins
+        self.lo, self.hi = shard_range(npoints, self.world, self.rank)
+        f64 = dict(dtype=torch.float64, device=device)
+        self.spectra = symm.empty((npoints, nbins), **f64)
+        self.chi2 = symm.empty((npoints,), **f64)
+        self.h_spec = symm.rendezvous(self.spectra, self.group)
+        self.h_chi2 = symm.rendezvous(self.chi2, self.group)
+        mc = bool(getattr(self.h_spec, "has_multicast_support", False)) and prefer_multicast
+        if callable(getattr(self.h_spec, "has_multicast_support", None)):
+            mc = bool(self.h_spec.has_multicast_support()) and prefer_multicast
+        self.multicast = mc and bool(self.h_spec.multicast_ptr) and bool(self.h_chi2.multicast_ptr)
+        self.root_only = not self.multicast
+
+    @staticmethod
+    def _base(h, tensor, multicast: bool, target_rank: int) -> int:
+        ptrs = list(h.buffer_ptrs)
+        off = tensor.data_ptr() - ptrs[h.rank]  # the tensor's offset in the symmetric buffer
+        return (h.multicast_ptr if multicast else ptrs[target_rank]) + off
+
+    def out_ptrs(self):
+        """(spectra rows ptr, chi2 ptr, flags) for this rank's rows."""
+        from . import GNA_OUT_MULTICAST, GNA_OUT_PEER
+        sb = self._base(self.h_spec, self.spectra, self.multicast, 0)
+        cb = self._base(self.h_chi2, self.chi2, self.multicast, 0)
+        flags = GNA_OUT_MULTICAST if self.multicast else GNA_OUT_PEER
+        return sb + self.lo * self.nbins * 8, cb + self.lo * 8, flags
+
+    def barrier(self):
+        """Device-side barrier on the current stream: every rank's remote writes are done."""
+        self.h_spec.barrier(channel=0)
+
+    def result(self):
+        """The gathered (spectra, chi2) as local tensors (all ranks with multicast, rank 0 else)."""
+        return self.spectra, self.chi2

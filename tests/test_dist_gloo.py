@@ -109,3 +109,34 @@ def test_shard_range_rejects_bad_args():
         gdist.shard_range(10, 0, 0)
     with pytest.raises(ValueError):
         gdist.shard_range(10, 2, 2)
+
+
+class _FakeHandle:
+    def __init__(self, rank, ptrs, mc):
+        self.rank, self.buffer_ptrs, self.multicast_ptr = rank, ptrs, mc
+
+
+class _FakeTensor:
+    def __init__(self, p):
+        self.p = p
+
+    def data_ptr(self):
+        return self.p
+
+
+def test_fused_gather_window_arithmetic():
+    """Row pointers of the fused-gather epilogue: tensor offset inside the symmetric buffer,
+    peer (root) vs multicast base, and this rank's first row."""
+    fg = gdist.FusedGather.__new__(gdist.FusedGather)
+    fg.npoints, fg.nbins, fg.world, fg.rank = 11, 7, 2, 1
+    fg.lo, fg.hi = gdist.shard_range(11, 2, 1)
+    fg.spectra, fg.chi2 = _FakeTensor(20_064), _FakeTensor(50_016)
+    fg.h_spec = _FakeHandle(1, [10_000, 20_000], 90_000)
+    fg.h_chi2 = _FakeHandle(1, [40_000, 50_000], 95_000)
+    for mc in (False, True):
+        fg.multicast = mc
+        sp, x2, flags = fg.out_ptrs()
+        base_s = (90_000 if mc else 10_000) + 64
+        base_c = (95_000 if mc else 40_000) + 16
+        assert sp == base_s + fg.lo * 7 * 8 and x2 == base_c + fg.lo * 8
+        assert flags == (2 if mc else 1)

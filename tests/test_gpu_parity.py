@@ -470,6 +470,49 @@ def test_repeated_calls_bitwise_deterministic(gna):
         assert np.array_equal(_np(gna.oscprob_eval(p, 52.5, E)), r0)
 
 
+# ------------------------------------------------------------------------ NEXT-4 fused gather
+def test_fused_gather_epilogue_single_rank(gna):
+    """gna_oscprob_batch_ex writing through symmetric memory (1-rank group on this one
+    GPU): peer-window stores and, where the fabric allows it, multicast stores give the
+    same bits as the plain batch."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1804_07682_b200 import dist as gdist
+    g = synth.rng(81)
+    pts, L, om, edges, data = _batch_case(g, 13, 3, 200, 10)
+    dp = {k: _t(v) for k, v in pts.items()}
+    de, dd = _t(edges), _t(data)
+    ref_sp, ref_x2 = gna.oscprob_batch(dp, L, om, de, 10, data=dd)
+    ref_sp, ref_x2 = _np(ref_sp).copy(), _np(ref_x2).copy()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % port, rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        modes = [False, True]
+        seen = []
+        for prefer_mc in modes:
+            fg = gdist.FusedGather(13, 200, "cuda", prefer_multicast=prefer_mc)
+            if prefer_mc and not fg.multicast:
+                continue
+            fg.spectra.fill_(float("nan"))
+            fg.chi2.fill_(float("nan"))
+            sp_ptr, x2_ptr, flags = fg.out_ptrs()
+            gna.oscprob_batch_ex(dp, L, om, de, 10, sp_ptr, x2_ptr, flags, data=dd)
+            fg.barrier()
+            sp, x2 = fg.result()
+            assert np.array_equal(_np(sp), ref_sp) and np.array_equal(_np(x2), ref_x2)
+            seen.append(flags)
+        assert gna.GNA_OUT_PEER in seen
+    finally:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------------ ABI on the GPU
 def test_host_pointer_to_device_entry_is_einval(gna):
     import ctypes
