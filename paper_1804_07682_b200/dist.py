@@ -180,10 +180,18 @@ class FusedGather:
         self.chi2 = symm.empty((npoints,), **f64)
         self.h_spec = symm.rendezvous(self.spectra, self.group)
         self.h_chi2 = symm.rendezvous(self.chi2, self.group)
-        mc = bool(getattr(self.h_spec, "has_multicast_support", False)) and prefer_multicast
-        if callable(getattr(self.h_spec, "has_multicast_support", None)):
-            mc = bool(self.h_spec.has_multicast_support()) and prefer_multicast
-        self.multicast = mc and bool(self.h_spec.multicast_ptr) and bool(self.h_chi2.multicast_ptr)
+        mc = False
+        if prefer_multicast:
+            from torch._C._distributed_c10d import _SymmetricMemory, DeviceType
+            dev = torch.device(device)
+            idx = dev.index if dev.index is not None else torch.cuda.current_device()
+            try:
+                mc = bool(_SymmetricMemory.has_multicast_support(DeviceType.CUDA, idx))
+            except (TypeError, RuntimeError):
+                mc = False
+        # the multicast window exists only if NVLS initialisation succeeded for both buffers
+        self.multicast = (mc and bool(self.h_spec.multicast_ptr)
+                          and bool(self.h_chi2.multicast_ptr))
         self.root_only = not self.multicast
 
     @staticmethod
