@@ -182,7 +182,8 @@ class FusedGather:
         self.h_chi2 = symm.rendezvous(self.chi2, self.group)
         mc = False
         if prefer_multicast:
-            from torch._C._distributed_c10d import _SymmetricMemory, DeviceType
+            from torch._C._autograd import DeviceType
+            from torch._C._distributed_c10d import _SymmetricMemory
             dev = torch.device(device)
             idx = dev.index if dev.index is not None else torch.cuda.current_device()
             try:
