@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--lib", default=None, help="alternative libgna_b200.so (tuning variants)")
+    ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "fused"],
+                    help="N>1 exchange: fused kernel-epilogue stores (validated) or NCCL all-gather")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as a CUDA graph (auto: when N == 1)")
     return ap.parse_args()
@@ -363,8 +365,42 @@ def main():
         def step():
             sb.step(compute, comm_stream=comm)
 
+        gather_mode = "none" if world == 1 else "nccl"
+        if world > 1 and args.gather in ("auto", "fused"):
+            # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
+            # validated bitwise against the NCCL gather before it is used
+            try:
+                fg = gdist.FusedGather(P, nb, dev)
+                sp_ptr, x2_ptr, fflags = fg.out_ptrs()
+
+                def step_fused():
+                    with KernelTimer(kern_ev):
+                        gna.oscprob_batch_ex(pts, L, om, edges, c["order"], sp_ptr, x2_ptr,
+                                             fflags, data=data, workspace=ws)
+                    fg.barrier()
+
+                step()
+                s_ref, x_ref = sb.gathered()
+                step_fused()
+                torch.cuda.synchronize()
+                ok = torch.ones(1, device=dev)
+                if rank == 0 or fg.multicast:
+                    same = bool(torch.equal(fg.spectra, s_ref)) and bool(torch.equal(fg.chi2, x_ref))
+                    ok.fill_(1.0 if same else 0.0)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                if float(ok) == 1.0:
+                    step = step_fused  # noqa: F811
+                    gather_mode = "fused-epilogue-" + ("multicast" if fg.multicast else "peer-to-root")
+                else:
+                    gather_mode = "nccl (fused epilogue failed bitwise validation)"
+                del s_ref, x_ref
+            except Exception as exc:  # noqa: BLE001 — fall back to the NCCL path, and say so
+                gather_mode = "nccl (fused epilogue unavailable: %s)" % str(exc).splitlines()[0][:120]
+            kern_ev.clear()
+
         units_per_rank = (hi - lo) * L.size * nb * c["order"]
-        calls_per_step = len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)])
+        calls_per_step = (1 if gather_mode.startswith("fused") else
+                          len([1 for a, b in sb.cb if min(b, sb.count) > min(a, sb.count)]))
         scaling = "strong"
     elif args.workload == "cfg4grid":
         grid = {k: torch.tensor(v, **f64) for k, v in c["grid"].items()}
@@ -565,6 +601,8 @@ def main():
             "bins_per_s": (c["bins_total"] * args.steps / (total_ms * 1e-3)) if c["bins_total"] else None,
             "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof,
             "cuda_graph": bool(use_graph)}
+    if args.workload in ("cfg4", "cfg5"):
+        line["config"]["gather"] = gather_mode
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
     if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu"):
