@@ -129,6 +129,13 @@ int gna_oscprob_eval_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, do
 int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges, int64_t nbins,
                      int32_t order, double* d_bins, void* stream);
 
+/* gna_gl_integrate_ab — NEXT-2 in binned form: per-bin Gauss-Legendre integrals of
+ * P(nu_alpha -> nu_beta) (the general formula of gna_oscprob_eval_ab).  Arguments and
+ * errors as gna_gl_integrate, plus EINVAL for alpha or beta outside [0, 2].          */
+int gna_gl_integrate_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, double L_km,
+                        const double* d_edges, int64_t nbins, int32_t order, double* d_bins,
+                        void* stream);
+
 /* ---------------------------------------------------------------------------
  * gna_oscprob_batch — batch over parameter points x baselines (BJ north_star):
  *   T[p][k]  = sum_{b<nbase} omega[b] * S_{p,b,k}       -> d_spectra[p*nbins+k]

@@ -59,6 +59,8 @@ def lib() -> ctypes.CDLL:
         L.oracle_gl_integrate.argtypes = [d, d, d, d, i, d, d, d, p, i64, i, p, i]
         L.oracle_gl_integrate.restype = i
         L.oracle_batch.argtypes = [p, p, p, p, i64, d, d, i, p, p, i, p, i64, i, p, p, p, i]
+        L.oracle_gl_integrate_ab.argtypes = [i, i, d, d, d, d, i, d, d, d, p, i64, i, p, i]
+        L.oracle_gl_integrate_ab.restype = i
         L.oracle_batch.restype = i
         L.oracle_max_threads.argtypes = []
         L.oracle_max_threads.restype = i
@@ -127,6 +129,20 @@ def gl_integrate(params: dict, L_km, edges, order: int, nthreads=1) -> np.ndarra
                                    params["delta_cp"], int(params.get("antineutrino", 0)),
                                    params["dm2_21"], params["dm2_31"], L_km, _ptr(edges),
                                    nbins, order, _ptr(bins), nthreads)
+    if rc < 0:
+        raise ValueError("bad order")
+    return bins
+
+
+def gl_integrate_ab(alpha, beta, params: dict, L_km, edges, order: int, nthreads=1) -> np.ndarray:
+    edges = _f64(edges)
+    nbins = edges.size - 1
+    bins = np.empty(max(nbins, 0))
+    rc = lib().oracle_gl_integrate_ab(alpha, beta, params["theta12"], params["theta13"],
+                                      params["theta23"], params["delta_cp"],
+                                      int(params.get("antineutrino", 0)), params["dm2_21"],
+                                      params["dm2_31"], L_km, _ptr(edges), nbins, order,
+                                      _ptr(bins), nthreads)
     if rc < 0:
         raise ValueError("bad order")
     return bins

@@ -242,6 +242,33 @@ int oracle_gl_integrate(double theta12, double theta13, double theta23, double d
 }
 
 /* ---------------------------------------------------------------------------
+ * Per-bin Gauss-Legendre integral of P(alpha -> beta) for any channel (the general
+ * formula of oracle_prob; binned as in oracle_gl_integrate):
+ *   S_k = h_k * sum_{i=0}^{n-1} w_i * P_ab(c_k + h_k t_i),  i ascending.
+ * ------------------------------------------------------------------------- */
+int oracle_gl_integrate_ab(int alpha, int beta, double theta12, double theta13, double theta23,
+                           double delta_cp, int antineutrino, double dm2_21, double dm2_31,
+                           double L_km, const double* edges, int64_t nbins, int order,
+                           double* bins, int nthreads) {
+  double t[64], w[64];
+  if (order < 1 || order > 64) return -1;
+  oracle_gauleg(order, t, w);
+  double complex V[9];
+  oracle_pmns(theta12, theta13, theta23, delta_cp, antineutrino, V);
+  int nt = set_threads(nthreads);
+#pragma omp parallel for schedule(static) num_threads(nt)
+  for (int64_t k = 0; k < nbins; ++k) {
+    double c = (edges[k] + edges[k + 1]) / 2.0;
+    double h = (edges[k + 1] - edges[k]) / 2.0;
+    double s = 0.0;
+    for (int i = 0; i < order; ++i)
+      s += w[i] * oracle_prob(alpha, beta, V, dm2_21, dm2_31, L_km, c + h * t[i]);
+    bins[k] = h * s;
+  }
+  return nt;
+}
+
+/* ---------------------------------------------------------------------------
  * Batch over parameter points and baselines (north_star "batched over
  * parameter points"; baseline merge = SPEC weighted_sum S:299-307 over the
  * one-E-node / m-OscProb topology S:431-439):

@@ -26,6 +26,7 @@ __all__ = [
     "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
     "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab", "oscprob_batch_ex",
+    "gl_integrate_ab",
     "GNA_OUT_PEER", "GNA_OUT_MULTICAST",
 ]
 
@@ -40,7 +41,7 @@ EXPORTS = (
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
     "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
-    "gna_oscprob_batch_ex",
+    "gna_oscprob_batch_ex", "gna_gl_integrate_ab",
 )
 
 GNA_OUT_PEER = 1
@@ -123,6 +124,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
                                        ctypes.c_uint32, vp]
     L.gna_oscprob_batch_ex.restype = ctypes.c_int
     L.gna_oscprob_eval_ab.restype = ctypes.c_int
+    L.gna_gl_integrate_ab.argtypes = [i32, i32, P, d, vp, i64, i32, vp, vp]
+    L.gna_gl_integrate_ab.restype = ctypes.c_int
     L.gna_oscprob_batch_workspace_size.argtypes = [i64, i32, i64, i32]
     L.gna_oscprob_batch_workspace_size.restype = sz
     L.gna_oscprob_batch.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
@@ -216,6 +219,22 @@ def oscprob_eval_ab(alpha: int, beta: int, params, L_km: float, E, out=None, str
     _check(L.gna_oscprob_eval_ab(int(alpha), int(beta), ctypes.byref(p), float(L_km),
                                  _dev(E, "E"), n, _dev(out, "out", n), _stream(stream)),
            "gna_oscprob_eval_ab")
+    return out
+
+
+def gl_integrate_ab(alpha: int, beta: int, params, L_km: float, edges, order: int, out=None,
+                    stream=None):
+    """Per-bin GL integrals of P(nu_alpha -> nu_beta) (gna_gl_integrate_ab, NEXT-2)."""
+    import torch
+    L = load()
+    nbins = edges.numel() - 1
+    if out is None:
+        out = torch.empty(max(nbins, 0), dtype=torch.float64, device=edges.device)
+    p = OscParams.of(params)._c()
+    _check(L.gna_gl_integrate_ab(int(alpha), int(beta), ctypes.byref(p), float(L_km),
+                                 _dev(edges, "edges"), nbins, int(order),
+                                 _dev(out, "out", max(nbins, 0)), _stream(stream)),
+           "gna_gl_integrate_ab")
     return out
 
 

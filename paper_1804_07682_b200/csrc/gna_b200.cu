@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
 // from a global (L1) copy of the table.
 constexpr int kGLLaneThreads = 128;
 
-template <int kOrder>
-__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c,
+template <int kOrder, class Coef>
+__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(Coef c,
                                                                  const double* __restrict__ edges,
                                                                  int64_t nbins,
                                                                  double* __restrict__ bins) {
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c,
     pv[i] = 0.0;
     if (node < kOrder)
       pv[i] = __ldg(&g_gl_w[off + node]) *
-              gna::pee_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
+              gna::prob_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
   }
   double s = 0.0;
 #pragma unroll
@@ -209,11 +209,12 @@ __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(PeeCoef c,
   if (act && half == 0) bins[k] = h * (s + other);
 }
 
-using gl_kernel_t = void (*)(PeeCoef, const double*, int64_t, double*);
+template <class Coef>
+using gl_kernel_t = void (*)(Coef, const double*, int64_t, double*);
 
-template <int... N>
-gl_kernel_t gl_kernel_for(int order, std::integer_sequence<int, N...>) {
-  static const gl_kernel_t t[] = {k_gl_integrate<N + 1>...};
+template <class Coef, int... N>
+gl_kernel_t<Coef> gl_kernel_for(int order, std::integer_sequence<int, N...>) {
+  static const gl_kernel_t<Coef> t[] = {k_gl_integrate<N + 1, Coef>...};
   return t[order - 1];
 }
 
@@ -904,11 +905,13 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
 
-int launch_gl(const PeeCoef& c, const double* edges, int64_t nbins, int order, double* bins,
+template <class Coef>
+int launch_gl(const Coef& c, const double* edges, int64_t nbins, int order, double* bins,
               cudaStream_t s) {
   const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
   if (grid > 0x7fffffffLL) return GNA_EINVAL;
-  const gl_kernel_t kern = gl_kernel_for(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+  const gl_kernel_t<Coef> kern =
+      gl_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
   kern<<<(unsigned)grid, kGLLaneThreads, 0, s>>>(c, edges, nbins, bins);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -1020,6 +1023,19 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
+  return launch_gl(c, d_edges, nbins, order, d_bins, (cudaStream_t)stream);
+}
+
+int gna_gl_integrate_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, double L_km,
+                        const double* d_edges, int64_t nbins, int32_t order, double* d_bins,
+                        void* stream) {
+  if (alpha < 0 || alpha > 2 || beta < 0 || beta > 2) return GNA_EINVAL;
+  int rc = validate_gl(p, L_km, d_edges, nbins, order, d_bins);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
+  gna::PabCoef c;
+  make_coef_ab(alpha, beta, p, L_km, &c);
   return launch_gl(c, d_edges, nbins, order, d_bins, (cudaStream_t)stream);
 }
 

@@ -96,6 +96,10 @@ def test_eval_ab_einval(lib, ab):
     # and the shared validation
     assert lib.gna_oscprob_eval_ab(0, 1, _params(), -1.0, BAD, 10, BAD2, None) == gna.GNA_EINVAL
     assert lib.gna_oscprob_eval_ab(0, 1, _params(), 1.0, BAD, 0, BAD2, None) == gna.GNA_EINVAL
+    assert lib.gna_gl_integrate_ab(ab[0], ab[1], _params(), 52.5, BAD, 10, 5, BAD2, None) == \
+        gna.GNA_EINVAL
+    assert lib.gna_gl_integrate_ab(0, 1, _params(), 52.5, BAD, 10, 33, BAD2, None) == \
+        gna.GNA_EINVAL
 
 
 def test_eval_null_params(lib):

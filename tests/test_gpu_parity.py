@@ -161,6 +161,25 @@ def test_eval_ab_all_channels_vs_oracle(gna, n):
         assert np.max(np.abs(M[0, 0] - Pee)) <= 1e-14
 
 
+@pytest.mark.parametrize("nbins,order", [(1, 1), (37, 5), (1000, 10), (100_003, 10), (50, 32)])
+def test_gl_integrate_ab_all_channels_vs_oracle(gna, nbins, order):
+    g = synth.rng(700 + nbins + order)
+    p = synth.random_params(g)
+    L = g.uniform(1, 300)
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    de = _t(edges)
+    tot = [np.zeros(nbins) for _ in range(3)]
+    for a in range(3):
+        for b in range(3):
+            S = _np(gna.gl_integrate_ab(a, b, p, L, de, order))
+            Sr = oracle.gl_integrate_ab(a, b, p, L, edges, order, nthreads=_nt())
+            # appearance bins can be ~0: absolute tolerance relative to the bin width
+            assert np.max(np.abs(S - Sr) / np.diff(edges)) <= TOL_BIN, (a, b)
+            tot[a] += S
+    for a in range(3):
+        assert np.max(np.abs(tot[a] / np.diff(edges) - 1)) <= 1e-12
+
+
 def test_eval_ab_cpt_and_L0(gna):
     g = synth.rng(61)
     p = synth.random_params(g)

@@ -396,3 +396,38 @@ def test_batch_is_weighted_sum_of_gl_integrals_and_chi2():
     # thread count does not change a bit
     S4, X4 = oracle.batch(pts, L, om, edges, 6, data=data, nthreads=3)
     assert np.array_equal(S, S4) and np.array_equal(X, X4)
+
+
+# ----------------------------------------------------------------------------- general-channel bins
+def test_gl_integrate_ab_ee_is_gl_integrate():
+    g = synth.rng(25)
+    p = synth.random_params(g)
+    e = np.sort(g.uniform(1.0, 10.0, 30))
+    assert np.array_equal(oracle.gl_integrate_ab(0, 0, p, 80.0, e, 7), oracle.gl_integrate(p, 80.0, e, 7))
+
+
+def test_gl_integrate_ab_unitarity_is_bin_width():
+    # sum_beta P(a->b) = 1 for every energy, so sum_beta S_ab = bin width
+    g = synth.rng(26)
+    for _ in range(5):
+        p = synth.random_params(g)
+        e = np.sort(g.uniform(1.0, 10.0, 25))
+        for a in range(3):
+            tot = sum(oracle.gl_integrate_ab(a, b, p, 120.0, e, 6)
+                      for b in range(3))
+            assert np.max(np.abs(tot / np.diff(e) - 1)) < 1e-13
+
+
+def test_gl_integrate_ab_brute_force_quadrature():
+    mp.mp.dps = 25
+    g = synth.rng(27)
+    p = synth.random_params(g)
+    L = 40.0
+    e0 = g.uniform(2.0, 8.0)
+    edges = np.sort(g.uniform(e0, e0 + 0.3, 3))
+    for a, b in ((0, 1), (1, 2), (2, 0)):
+        bins = oracle.gl_integrate_ab(a, b, p, L, edges, 32)
+        for k in range(2):
+            ref = mp.quad(lambda E: _mp_prob_evolution(a, b, p, L, E),
+                          mp.linspace(edges[k], edges[k + 1], 30))
+            assert abs(bins[k] - float(ref)) <= 1e-12 * max(abs(float(ref)), 1e-3)
