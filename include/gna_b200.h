@@ -189,6 +189,25 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
                          void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gna_fit_pattern_search — NEXT-4 (second part): a chi^2 minimiser that stays on the
+ * GPU (the minimisation of P:446-451), driving the batch kernels.  Deterministic
+ * compass search over x = (theta12, theta13, dm2_21, dm2_31): each iteration
+ * evaluates chi^2 of the 81 points x_c + s * {-1, 0, +1}^4 (baselines, bins, order
+ * and data as in gna_oscprob_batch), moves x_c to the argmin (lowest index on ties)
+ * or halves s when x_c is already best.  Everything is stream-ordered (no host
+ * synchronisation), so the niter iterations can be captured in one CUDA graph.
+ * d_state: device [8] = x_c[4] followed by s[4], updated in place.
+ * d_hist: device [niter] best chi^2 after each iteration, or NULL.
+ * d_workspace: >= gna_fit_workspace_size(nbase, nbins, order) bytes, 16-byte aligned.
+ * ------------------------------------------------------------------------- */
+size_t gna_fit_workspace_size(int32_t nbase, int64_t nbins, int32_t order);
+
+int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbase,
+                           const double* d_edges, int64_t nbins, int32_t order,
+                           const double* d_data, double* d_state, int32_t niter, double* d_hist,
+                           void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------
  * gna_oscprob_scan — separable grid scan (the paper's
  * "computed only once ... re-computed only if any of the variables or inputs it
  * depends on were modified", and one transformation per formula item,

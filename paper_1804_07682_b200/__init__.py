@@ -26,7 +26,7 @@ __all__ = [
     "oscprob_batch_host", "gl_rule",
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
     "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab", "oscprob_batch_ex",
-    "gl_integrate_ab",
+    "gl_integrate_ab", "fit_pattern_search", "fit_workspace_size",
     "GNA_OUT_PEER", "GNA_OUT_MULTICAST",
 ]
 
@@ -41,7 +41,8 @@ EXPORTS = (
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
     "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
-    "gna_oscprob_batch_ex", "gna_gl_integrate_ab",
+    "gna_oscprob_batch_ex", "gna_gl_integrate_ab", "gna_fit_workspace_size",
+    "gna_fit_pattern_search",
 )
 
 GNA_OUT_PEER = 1
@@ -126,6 +127,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_oscprob_eval_ab.restype = ctypes.c_int
     L.gna_gl_integrate_ab.argtypes = [i32, i32, P, d, vp, i64, i32, vp, vp]
     L.gna_gl_integrate_ab.restype = ctypes.c_int
+    L.gna_fit_workspace_size.argtypes = [i32, i64, i32]
+    L.gna_fit_workspace_size.restype = sz
+    L.gna_fit_pattern_search.argtypes = [vp, vp, i32, vp, i64, i32, vp, vp, i32, vp, vp, sz, vp]
+    L.gna_fit_pattern_search.restype = ctypes.c_int
     L.gna_oscprob_batch_workspace_size.argtypes = [i64, i32, i64, i32]
     L.gna_oscprob_batch_workspace_size.restype = sz
     L.gna_oscprob_batch.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz, vp]
@@ -354,6 +359,31 @@ def oscprob_batch_ex(points: dict, L_km, omega, edges, order: int, spectra_ptr: 
         int(order), spectra_ptr, _dev(data, "data", nbins) if data is not None else None,
         chi2_ptr, _dev(workspace, "workspace"), workspace.numel() * 8, int(flags),
         _stream(stream)), "gna_oscprob_batch_ex")
+
+
+def fit_workspace_size(nbase: int, nbins: int, order: int) -> int:
+    return int(load().gna_fit_workspace_size(int(nbase), int(nbins), int(order)))
+
+
+def fit_pattern_search(state, L_km, omega, edges, order: int, data, niter: int, hist=None,
+                       workspace=None, stream=None):
+    """On-GPU chi^2 pattern search (gna_fit_pattern_search).  state: CUDA float64 [8] =
+    centre (theta12, theta13, dm2_21, dm2_31) + steps, updated in place; returns hist."""
+    import torch
+    L = load()
+    nbins = edges.numel() - 1
+    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    if hist is None and niter > 0:
+        hist = torch.empty(niter, dtype=torch.float64, device=edges.device)
+    if workspace is None:
+        wb = fit_workspace_size(Lh.size, nbins, order)
+        workspace = torch.empty(max(wb // 8, 2), dtype=torch.float64, device=edges.device)
+    _check(L.gna_fit_pattern_search(
+        Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins, int(order),
+        _dev(data, "data", nbins), _dev(state, "state", 8), int(niter),
+        _dev(hist, "hist", niter) if hist is not None else None, _dev(workspace, "workspace"),
+        workspace.numel() * 8, _stream(stream)), "gna_fit_pattern_search")
+    return hist
 
 
 # ---------------------------------------------------------------- host-buffer entry points

@@ -632,6 +632,64 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
 }
 
 // ----------------------------------------------------------------------------
+// NEXT-4 (second part): a chi^2 minimiser that stays on the GPU (the fit of P:446-451).
+// Deterministic compass/pattern search over (theta12, theta13, dm2_21, dm2_31): every
+// iteration evaluates the 3^4 = 81 points centre + step * {-1, 0, +1}^4 with the batch
+// kernels (chi^2 only), takes the argmin (lowest index on ties), moves the centre there,
+// or halves the steps if the centre is already best.  The whole loop is stream-ordered
+// (no host round trip), so it can be captured in one CUDA graph.
+constexpr int kFitDim = 4;
+constexpr int kFitCand = 81;  // 3^4
+
+// state = {centre[4], step[4]} (device, fp64)
+__global__ void __launch_bounds__(128) k_fit_candidates(const double* __restrict__ state,
+                                                        double* __restrict__ cand) {
+  const int c = threadIdx.x;
+  if (c >= kFitCand) return;
+  int code = c;
+#pragma unroll
+  for (int d = 0; d < kFitDim; ++d) {
+    const int o = code % 3 - 1;  // -1, 0, +1 ; candidate 40 is the centre
+    code /= 3;
+    cand[d * kFitCand + c] = fma((double)o, state[kFitDim + d], state[d]);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_fit_update(double* __restrict__ state,
+                                                    const double* __restrict__ cand,
+                                                    const double* __restrict__ chi2,
+                                                    double* __restrict__ hist, int iter) {
+  __shared__ double s_v[128];
+  __shared__ int s_i[128];
+  const int t = threadIdx.x;
+  s_v[t] = t < kFitCand ? chi2[t] : INFINITY;
+  s_i[t] = t;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {  // argmin, ties -> lowest index (deterministic)
+    if (t < o) {
+      const double a = s_v[t], b = s_v[t + o];
+      if (b < a || (b == a && s_i[t + o] < s_i[t])) {
+        s_v[t] = b;
+        s_i[t] = s_i[t + o];
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const int best = s_i[0];
+    const int centre = kFitCand / 2;
+    if (best == centre || !(s_v[0] < chi2[centre])) {
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[kFitDim + d] *= 0.5;
+    } else {
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[d] = cand[d * kFitCand + best];
+    }
+    if (hist) hist[iter] = fmin(s_v[0], chi2[centre]);
+  }
+}
+
+// ----------------------------------------------------------------------------
 // host helpers
 // ----------------------------------------------------------------------------
 int cuda_fail(cudaError_t e) {
@@ -1151,6 +1209,52 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_scan(g, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
                      d_workspace, (cudaStream_t)stream);
+}
+
+size_t gna_fit_workspace_size(int32_t nbase, int64_t nbins, int32_t order) {
+  if (nbase < 1 || nbase > GNA_MAX_NBASE || nbins < 1 || order < 1 || order > GNA_MAX_ORDER)
+    return 0;
+  return align16((size_t)kFitDim * kFitCand * 8) + align16((size_t)kFitCand * 8) +
+         batch_ws_bytes(kFitCand, nbase, nbins, order, true);
+}
+
+int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbase,
+                           const double* d_edges, int64_t nbins, int32_t order,
+                           const double* d_data, double* d_state, int32_t niter, double* d_hist,
+                           void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (!L_km || !omega || nbase < 1 || nbase > GNA_MAX_NBASE || !d_edges || nbins < 1 ||
+      order < 1 || order > GNA_MAX_ORDER || !d_data || !d_state || niter < 0 || !d_workspace ||
+      ((uintptr_t)d_workspace & 15) ||
+      workspace_bytes < gna_fit_workspace_size(nbase, nbins, order))
+    return GNA_EINVAL;
+  for (int b = 0; b < nbase; ++b)
+    if (!is_fin(L_km[b]) || L_km[b] < 0 || !is_fin(omega[b])) return GNA_EINVAL;
+  int rc;
+  if ((rc = check_device())) return rc;
+  const void* ptrs[5] = {d_edges, d_data, d_state, d_hist, d_workspace};
+  for (const void* q : ptrs)
+    if (q && check_dev_ptr(q)) return GNA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  char* w = (char*)d_workspace;
+  double* cand = (double*)w;
+  w += align16((size_t)kFitDim * kFitCand * 8);
+  double* chi2 = (double*)w;
+  w += align16((size_t)kFitCand * 8);
+  void* bws = w;
+  const gna_param_batch pts = {cand, cand + kFitCand, cand + 2 * kFitCand, cand + 3 * kFitCand,
+                               kFitCand};
+  for (int it = 0; it < niter; ++it) {
+    k_fit_candidates<<<1, 128, 0, s>>>(d_state, cand);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if ((rc = launch_batch(&pts, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data,
+                           chi2, bws, s)))
+      return rc;
+    k_fit_update<<<1, 128, 0, s>>>(d_state, cand, chi2, d_hist, it);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return GNA_OK;
 }
 
 int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const double* omega,

@@ -186,6 +186,23 @@ def test_scan_workspace_size(lib):
     assert w >= 100 * 3 * 1000 * 8 + 2 * 1000 * 8 + 100 * 32 and w % 32 == 0
 
 
+def test_fit_einval(lib):
+    L = np.array([52.5])
+    om = np.ones(1)
+    args = dict(L=L.ctypes.data, om=om.ctypes.data, nbase=1, edges=0x500000, nbins=10, order=5,
+                data=0x700000, state=0x800000, niter=5, hist=None, ws=0x900000, wsb=1 << 20)
+    def call(**kw):
+        a = dict(args, **kw)
+        return lib.gna_fit_pattern_search(a["L"], a["om"], a["nbase"], a["edges"], a["nbins"],
+                                          a["order"], a["data"], a["state"], a["niter"],
+                                          a["hist"], a["ws"], a["wsb"], None)
+    for kw in (dict(L=None), dict(nbase=0), dict(edges=None), dict(nbins=0), dict(order=40),
+               dict(data=None), dict(state=None), dict(niter=-1), dict(ws=None), dict(wsb=8),
+               dict(ws=0x900008)):
+        assert call(**kw) == gna.GNA_EINVAL, kw
+    assert gna.fit_workspace_size(1, 10, 5) > 0 and gna.fit_workspace_size(0, 10, 5) == 0
+
+
 def test_batch_workspace_size(lib):
     assert gna.oscprob_batch_workspace_size(0, 1, 10, 5) == 0
     assert gna.oscprob_batch_workspace_size(10, 1, 0, 5) == 0

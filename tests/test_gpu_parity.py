@@ -532,6 +532,51 @@ def test_fused_gather_epilogue_single_rank(gna):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------------ on-GPU fit loop
+def _fit_case():
+    truth = np.array([0.5838, 0.1496, 7.53e-5, 2.52e-3])
+    L, om = np.array([52.5, 215.0]), np.array([1.0, 0.0596])
+    edges = synth.uniform_edges(500, 1.0, 10.0)
+    pts = dict(theta12=truth[:1], theta13=truth[1:2], dm2_21=truth[2:3], dm2_31=truth[3:4])
+    data, _ = oracle.batch(pts, L, om, edges, 5, nthreads=_nt())  # pseudo-data = oracle at truth
+    return truth, L, om, edges, data[0]
+
+
+def test_fit_pattern_search_recovers_truth(gna):
+    truth, L, om, edges, data = _fit_case()
+    step = np.array([0.01, 0.005, 2e-6, 5e-5])
+    start = truth + np.array([3.1, -2.2, 2.7, -3.3]) * step
+    state = _t(np.r_[start, step])
+    hist = _np(gna.fit_pattern_search(state, L, om, _t(edges), 5, _t(data), 120))
+    x = _np(state)[:4]
+    assert np.all(np.diff(hist) <= 0)          # best chi^2 never increases
+    assert hist[-1] < 1e-12 * hist[0]
+    assert np.all(np.abs(x - truth) <= 1e-6 * np.abs(truth)), (x, truth)
+
+
+def test_fit_pattern_search_deterministic_and_graph_capturable(gna):
+    import torch
+    truth, L, om, edges, data = _fit_case()
+    step = np.array([0.01, 0.005, 2e-6, 5e-5])
+    s0 = np.r_[truth + 2 * step, step]
+    de, dd = _t(edges), _t(data)
+    a = _t(s0)
+    gna.fit_pattern_search(a, L, om, de, 5, dd, 30)
+    b = _t(s0)
+    ws = torch.empty(gna.fit_workspace_size(2, 500, 5) // 8 + 2, dtype=torch.float64, device="cuda")
+    hist = torch.empty(30, dtype=torch.float64, device="cuda")
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            gna.fit_pattern_search(b, L, om, de, 5, dd, 30, hist=hist, workspace=ws)
+    torch.cuda.current_stream().wait_stream(s)
+    b.copy_(_t(s0))
+    graph.replay()
+    assert np.array_equal(_np(a), _np(b))
+
+
 # ------------------------------------------------------------------------ ABI on the GPU
 def test_host_pointer_to_device_entry_is_einval(gna):
     import ctypes
