@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg4", "cfg3", "cfg2", "cfg1",
-                                                            "cfg4grid", "cfg3emu"])
+                                                            "cfg4grid", "cfg3emu", "cfg5fit"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chunks", type=int, default=0, help="gather pipeline chunks (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -68,8 +68,22 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- workloads
+FIT_ITERS = 50
+
+
 def workload(name: str) -> dict:
-    c = synth.config("cfg3" if name == "cfg3emu" else name)
+    c = synth.config({"cfg3emu": "cfg3", "cfg5fit": "cfg5"}.get(name, name))
+    if name == "cfg5fit":
+        nb = c["edges"].size - 1
+        c["evals"] = FIT_ITERS * 81 * c["L_km"].size * nb * c["order"]
+        c["bins_total"] = FIT_ITERS * 81 * nb
+        c["desc"] = dict(workload="cfg5fit: on-GPU chi^2 pattern-search fit (NEXT-4), %d "
+                         "iterations x 81 candidate points on the cfg5 geometry (8 baselines x "
+                         "%d energies), one CUDA graph per fit" % (FIT_ITERS, nb * c["order"]),
+                         points=81 * FIT_ITERS, baselines=int(c["L_km"].size), bins=nb,
+                         order=c["order"])
+        c["name"] = name
+        return c
     if name == "cfg3emu":
         c["params"] = dict(c["params"], delta_cp=1.2)
     if name in ("cfg4", "cfg5"):
@@ -321,6 +335,8 @@ def main():
         print("run N>1 under torchrun (WORLD_SIZE unset)", file=sys.stderr)
         sys.exit(2)
     if args.impl == "reference":
+        if args.workload == "cfg5fit":
+            args.workload = "cfg5"  # the oracle has no fit loop: time its batch evaluation
         return run_reference(args, rank, world)
 
     import torch
@@ -450,6 +466,26 @@ def main():
         units_per_rank = c["evals"]
         calls_per_step = 1
         scaling = "weak"  # replicas only
+    elif args.workload == "cfg5fit":
+        edges = torch.tensor(c["edges"], **f64)
+        data = torch.tensor(c["data"], **f64)
+        nb = c["edges"].size - 1
+        start = np.array([0.5838, 0.1496, 7.53e-5, 2.52e-3, 0.01, 0.005, 2e-6, 5e-5])
+        state = torch.tensor(start, **f64)
+        state0 = torch.tensor(start, **f64)
+        hist = torch.empty(FIT_ITERS, **f64)
+        ws = torch.empty(gna.fit_workspace_size(c["L_km"].size, nb, c["order"]) // 8 + 2, **f64)
+        kern_ev = []
+
+        def step():
+            state.copy_(state0)
+            with KernelTimer(kern_ev):
+                gna.fit_pattern_search(state, c["L_km"], c["omega"], edges, c["order"], data,
+                                       FIT_ITERS, hist=hist, workspace=ws)
+
+        units_per_rank = c["evals"]
+        calls_per_step = FIT_ITERS
+        scaling = "weak"  # replicas only (one fit per GPU)
     elif args.workload == "cfg3emu":
         E = torch.linspace(c["lo"], c["hi"], c["n"], **f64)
         out = torch.empty_like(E)
@@ -605,14 +641,15 @@ def main():
         line["config"]["gather"] = gather_mode
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
-    if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu"):
+    if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu", "cfg5fit"):
         line["e2e"] = e2e(args, c, gna, torch, dist, dev, world, rank, local)
-    elif args.workload in ("cfg4grid", "cfg3emu"):
+    elif args.workload in ("cfg4grid", "cfg3emu", "cfg5fit"):
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0, "note": "no host-buffer variant for this NEXT row yet"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(c, args.workload, args.cpu_seconds)
+        line["cpu_baseline"] = cpu_baseline(c, "cfg5" if args.workload == "cfg5fit" else
+                                            args.workload, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
