@@ -308,6 +308,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 #define GNA_PRAGMA(x) _Pragma(#x)
 #define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
+#ifndef GNA_BATCH_PI
+#define GNA_BATCH_PI 1
+#endif
 #ifndef GNA_BATCH_LDS_PREFETCH
 #define GNA_BATCH_LDS_PREFETCH 0
 #endif
@@ -432,6 +435,83 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     }
   }
   if constexpr (kOut != kOutLocal) __threadfence_system();  // remote stores before completion
+}
+
+// Small-nbase variant (few terms per node, several points per warp, e.g. cfg4's
+// single-baseline scan): the loops are interchanged so the node group is outer and the
+// warp's points inner — 1/E and h*w of a node group are loaded once for all ppw points
+// instead of once per point.  Per point the node sums are accumulated in the same order
+// as k_oscprob_batch, so the results are bitwise identical.
+constexpr int kMaxPPW = 16;
+
+template <int N, int kOut>
+__global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
+    int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
+    double* __restrict__ spectra, const double* __restrict__ data) {
+  extern __shared__ double2 s_dyn[];
+  double2* sc = s_dyn;                                          // [ppw][nterm]
+  double* s_acc = reinterpret_cast<double*>(s_dyn + ppw * nterm);  // [ppw][32]
+  double* s_c0 = s_acc + ppw * 32;                               // [ppw]
+  const int lane = threadIdx.x & 31;
+  const int64_t pg = blockIdx.x / bpp;
+  const int64_t wt = blockIdx.x - pg * bpp;
+  const int64_t k0 = wt * 32;
+  if (k0 >= nbins) return;
+  const int64_t p0 = pg * (int64_t)ppw;
+  const int np = (int)min((int64_t)ppw, npoints - p0);
+  for (int j = lane; j < np * nterm; j += 32) sc[j] = w.coef[p0 * nterm + j];
+  for (int j = lane; j < np; j += 32) s_c0[j] = w.c0[p0 + j];
+  for (int q = 0; q < np; ++q) s_acc[q * 32 + lane] = 0.0;
+  __syncwarp();
+  const int64_t k = k0 + lane;
+  const bool active = k < nbins;
+  const int64_t kk = active ? k : nbins - 1;
+  const double* __restrict__ invE = w.invE + kk;
+  const double* __restrict__ hw = w.hw + kk;
+  for (int i = 0; i < order; i += N) {
+    const int nn = min(N, order - i);
+    double iE[N], hv[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      iE[n] = n < nn ? invE[(int64_t)(i + n) * nbins] : 1.0;
+      hv[n] = n < nn ? hw[(int64_t)(i + n) * nbins] : 0.0;
+    }
+    for (int q = 0; q < np; ++q) {
+      const double2* __restrict__ cq = sc + q * nterm;
+      double a[N];
+#pragma unroll
+      for (int n = 0; n < N; ++n) a[n] = 0.0;
+      for (int j = 0; j < nterm; ++j) {
+        const double2 cw = cq[j];
+#pragma unroll
+        for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+      }
+      const double c0 = s_c0[q];
+      double sv = s_acc[q * 32 + lane];
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < nn) sv = fma(hv[n], c0 - a[n], sv);
+      s_acc[q * 32 + lane] = sv;
+    }
+  }
+  const double D = (data && active) ? data[k] : 1.0;
+  const int64_t wpp = warps_per_point_dev(nbins);
+  for (int q = 0; q < np; ++q) {
+    const int64_t p = p0 + q;
+    const double sv = s_acc[q * 32 + lane];
+    double x2 = 0.0;
+    if (active) {
+      if (spectra) out_store<kOut>(spectra + p * nbins + k, sv);
+      const double d = sv - D;
+      x2 = d * d / D;
+    }
+    if (w.partial) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
+    }
+  }
+  if constexpr (kOut != kOutLocal) __threadfence_system();
 }
 
 // chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
@@ -898,8 +978,21 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut>
               : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut>
                                  : k_oscprob_batch<kBatchWarps, 4, kOut>;
-  kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
-      nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
+  if (ppw > 1 && kBatchWarps == 1 && GNA_BATCH_PI) {
+    // several points per warp: node groups outer, points inner (bitwise-identical sums)
+    ppw = std::min<int64_t>(ppw, kMaxPPW);
+    const int64_t ng = (pts->npoints + ppw - 1) / ppw;
+    const size_t smem_pi = (size_t)ppw * nterm * sizeof(double2) + (size_t)ppw * 33 * 8;
+    auto kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut>
+               : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut>
+               : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut>
+                                  : k_oscprob_batch_pi<4, kOut>;
+    kpi<<<(unsigned)(ng * bpp), 32, smem_pi, s>>>(nterm, order, nbins, pts->npoints, bpp,
+                                                  (int)ppw, w, spectra, chi2 ? data : nullptr);
+  } else {
+    kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
+        nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);

@@ -309,6 +309,18 @@ def test_batch_small_vs_oracle(gna, P, nbase, nbins, order):
     assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
+@pytest.mark.parametrize("order", [10, 7])
+def test_batch_points_inner_path_vs_oracle(gna, order):
+    """Single baseline, many points: the launcher packs several points per warp and runs
+    the node-outer/points-inner kernel; all points compared with the oracle."""
+    g = synth.rng(90 + order)
+    pts, L, om, edges, data = _batch_case(g, 2003, 1, 1000, order)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data)
+    spr, x2r = oracle.batch(pts, L, om, edges, order, data=data, nthreads=_nt())
+    assert np.max(np.abs(sp - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2 - x2r) <= _chi2_bound(spr, data))
+
+
 def test_batch_single_baseline_matches_gl_integrate(gna):
     g = synth.rng(41)
     pts, _, _, edges, _ = _batch_case(g, 4, 1, 200, 10)

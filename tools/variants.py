@@ -12,9 +12,8 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "b_base": dict(),
-    "b_small1": dict(GNA_BATCH_SMALL_NBASE=1),
-    "b_small8": dict(GNA_BATCH_SMALL_NBASE=8),
+    "pi0": dict(GNA_BATCH_PI=0),
+    "pi1": dict(GNA_BATCH_PI=1),
 }
 
 
@@ -27,7 +26,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_batchILi1ELi10E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_batch_piILi5ELi0E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
