@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI
 #define GNA_BATCH_PI 1
 #endif
+#ifndef GNA_BATCH_PPW_WORK
+#define GNA_BATCH_PPW_WORK 240
+#endif
 #ifndef GNA_BATCH_LDS_PREFETCH
 #define GNA_BATCH_LDS_PREFETCH 0
 #endif
@@ -957,7 +960,7 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   // points per warp: enough sin^2 work per lane (>= ~240) to amortise the per-point
   // overhead, while keeping >= 16 warps per SM worth of blocks
   const int64_t work = (int64_t)3 * nbase * order;
-  int64_t ppw = std::max<int64_t>(1, (240 + work - 1) / work);
+  int64_t ppw = std::max<int64_t>(1, (GNA_BATCH_PPW_WORK + work - 1) / work);
   const int64_t min_blocks = (int64_t)sm_count() * 16;
   while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
   const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;

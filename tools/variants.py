@@ -12,8 +12,10 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "pi0": dict(GNA_BATCH_PI=0),
-    "pi1": dict(GNA_BATCH_PI=1),
+    "ppw240": dict(GNA_BATCH_PPW_WORK=240),
+    "ppw480": dict(GNA_BATCH_PPW_WORK=480),
+    "ppw960": dict(GNA_BATCH_PPW_WORK=960),
+    "ppw120": dict(GNA_BATCH_PPW_WORK=120),
 }
 
 
