@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI
 #define GNA_BATCH_PI 1
 #endif
+#ifndef GNA_BATCH_PI_Q2
+#define GNA_BATCH_PI_Q2 0
+#endif
 #ifndef GNA_BATCH_PPW_WORK
 #define GNA_BATCH_PPW_WORK 240
 #endif
@@ -479,7 +482,36 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
       iE[n] = n < nn ? invE[(int64_t)(i + n) * nbins] : 1.0;
       hv[n] = n < nn ? hw[(int64_t)(i + n) * nbins] : 0.0;
     }
-    for (int q = 0; q < np; ++q) {
+    int q = 0;
+#if GNA_BATCH_PI_Q2
+    // two points at a time: 2N independent sin^2 chains per coefficient step
+    for (; q + 1 < np; q += 2) {
+      const double2* __restrict__ cq = sc + q * nterm;
+      const double2* __restrict__ cr = cq + nterm;
+      double a[N], b[N];
+#pragma unroll
+      for (int n = 0; n < N; ++n) a[n] = b[n] = 0.0;
+      for (int j = 0; j < nterm; ++j) {
+        const double2 cw = cq[j], cv = cr[j];
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+          b[n] = fma(cv.y, gna::sin2c(cv.x, iE[n]), b[n]);
+        }
+      }
+      const double c0a = s_c0[q], c0b = s_c0[q + 1];
+      double sa = s_acc[q * 32 + lane], sb = s_acc[(q + 1) * 32 + lane];
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < nn) {
+          sa = fma(hv[n], c0a - a[n], sa);
+          sb = fma(hv[n], c0b - b[n], sb);
+        }
+      s_acc[q * 32 + lane] = sa;
+      s_acc[(q + 1) * 32 + lane] = sb;
+    }
+#endif
+    for (; q < np; ++q) {
       const double2* __restrict__ cq = sc + q * nterm;
       double a[N];
 #pragma unroll

@@ -12,10 +12,10 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "ppw240": dict(GNA_BATCH_PPW_WORK=240),
-    "ppw480": dict(GNA_BATCH_PPW_WORK=480),
-    "ppw960": dict(GNA_BATCH_PPW_WORK=960),
-    "ppw120": dict(GNA_BATCH_PPW_WORK=120),
+    "q1": dict(GNA_BATCH_PI_Q2=0),
+    "q2": dict(GNA_BATCH_PI_Q2=1),
+    "q2n4": dict(GNA_BATCH_PI_Q2=1),
+    "q2_480": dict(GNA_BATCH_PI_Q2=1, GNA_BATCH_PPW_WORK=480),
 }
 
 
