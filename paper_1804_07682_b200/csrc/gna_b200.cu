@@ -312,10 +312,10 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #define GNA_BATCH_PI 1
 #endif
 #ifndef GNA_BATCH_PI_Q2
-#define GNA_BATCH_PI_Q2 0
+#define GNA_BATCH_PI_Q2 1
 #endif
 #ifndef GNA_BATCH_PPW_WORK
-#define GNA_BATCH_PPW_WORK 240
+#define GNA_BATCH_PPW_WORK 480
 #endif
 #ifndef GNA_BATCH_LDS_PREFETCH
 #define GNA_BATCH_LDS_PREFETCH 0
