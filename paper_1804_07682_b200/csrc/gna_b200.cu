@@ -615,9 +615,10 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
   return w;
 }
 
-// stage A: thread per (mass point c, pair ij, bin k) -> G[c][ij][k]; threads with
-// c == 0, ij == 0 also write H[k] and 1/D[k]; extra threads compute the mixing
-// weights of each mixing point.
+// stage A: thread per (mass point c, bin k): the three pairs share each node's
+// reciprocal and run as three independent sin^2 chains (two nodes per iteration:
+// six chains) -> G[c][*][k]; threads with c == 0 also write H[k] and 1/D[k]; extra
+// threads compute the mixing weights of each mixing point.
 __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
                                                     const double* __restrict__ th13,
                                                     const double* __restrict__ d21,
@@ -625,12 +626,10 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
                                                     const double* __restrict__ edges,
                                                     const double* __restrict__ data, ScanWs w) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n1 = a.nmass * 3 * a.nbins;
+  const int64_t n1 = a.nmass * a.nbins;
   if (t < n1) {
-    const int64_t row = t / a.nbins;  // c * 3 + ij
-    const int64_t k = t - row * a.nbins;
-    const int64_t c = row / 3;
-    const int ij = (int)(row - c * 3);
+    const int64_t c = t / a.nbins;
+    const int64_t k = t - c * a.nbins;
     const int off = GNA_GL_OFF(a.order);
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
@@ -638,19 +637,32 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
     double wsum = 0.0;
     for (int i = 0; i < a.order; ++i) wsum += c_gl_w[off + i];
     const double m21 = d21[c], m31 = d31[c];
-    const double m = ij == 0 ? m21 : (ij == 1 ? m31 : m31 - m21);
-    double G = 0.0;
+    const double m32 = m31 - m21;
+    double G0 = 0.0, G1 = 0.0, G2 = 0.0;
     for (int b = 0; b < a.nbase; ++b) {
-      const double kq = phase_slope(m, a.L[b]);
-      double s = 0.0;
+      const double k0 = phase_slope(m21, a.L[b]);
+      const double k1 = phase_slope(m31, a.L[b]);
+      const double k2 = phase_slope(m32, a.L[b]);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll 2
-      for (int i = 0; i < a.order; ++i)
-        s = fma(c_gl_w[off + i], gna::sin2c(kq, gna::rcp(fma(h, c_gl_t[off + i], ctr))), s);
+      for (int i = 0; i < a.order; ++i) {
+        const double invE = gna::rcp(fma(h, c_gl_t[off + i], ctr));
+        const double wi = c_gl_w[off + i];
+        s0 = fma(wi, gna::sin2c(k0, invE), s0);
+        s1 = fma(wi, gna::sin2c(k1, invE), s1);
+        s2 = fma(wi, gna::sin2c(k2, invE), s2);
+      }
       // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
-      G = fma(a.omega[b] * h, fma(0.5, wsum, s), G);
+      const double ob = a.omega[b] * h;
+      G0 = fma(ob, fma(0.5, wsum, s0), G0);
+      G1 = fma(ob, fma(0.5, wsum, s1), G1);
+      G2 = fma(ob, fma(0.5, wsum, s2), G2);
     }
-    w.G[t] = G;
-    if (row == 0) {
+    double* g = w.G + (c * 3) * a.nbins + k;
+    g[0] = G0;
+    g[a.nbins] = G1;
+    g[2 * a.nbins] = G2;
+    if (c == 0) {
       w.H[k] = a.omega_sum * h * wsum;
       if (data) w.invD[k] = 1.0 / data[k];
     }
@@ -1075,7 +1087,7 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   a.nmix = g->nmix;
   a.nmass = g->nmass;
   const ScanWs w = scan_ws_carve(workspace, g->nmix, g->nmass, nbins);
-  const int64_t nsetup = g->nmass * 3 * nbins + g->nmix;
+  const int64_t nsetup = g->nmass * nbins + g->nmix;
   const int64_t nchunk = (g->nmix + kScanA - 1) / kScanA;
   const int64_t nblk = g->nmass * nchunk;
   if ((nsetup + 127) / 128 > 0x7fffffffLL || nblk > 0x7fffffffLL) return GNA_EINVAL;
