@@ -314,6 +314,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI_Q2
 #define GNA_BATCH_PI_Q2 1
 #endif
+#ifndef GNA_BATCH_PI_MAX_TERMS
+#define GNA_BATCH_PI_MAX_TERMS 6
+#endif
 #ifndef GNA_BATCH_PPW_WORK
 #define GNA_BATCH_PPW_WORK 480
 #endif
@@ -1001,10 +1004,12 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   a.npoints = pts->npoints;
   const BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
   const int64_t bpp = blocks_per_point(nbins);
-  // points per warp: enough sin^2 work per lane (>= ~240) to amortise the per-point
-  // overhead, while keeping >= 16 warps per SM worth of blocks
+  // points per warp: enough sin^2 work per lane to amortise the per-point overhead
+  // (>= 240; >= GNA_BATCH_PPW_WORK for the small-nbase points-inner kernel), while
+  // keeping >= 16 warps per SM worth of blocks
   const int64_t work = (int64_t)3 * nbase * order;
-  int64_t ppw = std::max<int64_t>(1, (GNA_BATCH_PPW_WORK + work - 1) / work);
+  const bool small_terms = 3 * nbase <= GNA_BATCH_PI_MAX_TERMS;
+  int64_t ppw = std::max<int64_t>(1, ((small_terms ? GNA_BATCH_PPW_WORK : 240) + work - 1) / work);
   const int64_t min_blocks = (int64_t)sm_count() * 16;
   while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
   const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;
@@ -1025,7 +1030,7 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut>
               : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut>
                                  : k_oscprob_batch<kBatchWarps, 4, kOut>;
-  if (ppw > 1 && kBatchWarps == 1 && GNA_BATCH_PI) {
+  if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
     // several points per warp: node groups outer, points inner (bitwise-identical sums)
     ppw = std::min<int64_t>(ppw, kMaxPPW);
     const int64_t ng = (pts->npoints + ppw - 1) / ppw;
