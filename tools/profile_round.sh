@@ -20,7 +20,7 @@ prof() {  # name workload kernel-regex
         -o gpurun_out/final/prof_$1 $B > gpurun_out/final/ncu_$1.log 2>&1
   echo "prof $1 rc=$?"
 }
-prof batch cfg5 'k_oscprob_batch<'
+prof batch cfg5 '^k_oscprob_batch$'
 prof batch_pi cfg4 k_oscprob_batch_pi
 prof eval cfg3 k_oscprob_eval_tma
 prof eval_ab cfg3emu k_oscprob_eval_tma
