@@ -1,0 +1,357 @@
+// k_batch.cuh — (a1)-(a5) batch kernels: setup, per-point / points-inner main pass, chi2 reduce
+// Part of libgna_b200.so: included once, from gna_b200.cu (single translation unit).
+#pragma once
+#include "gna_common.cuh"
+
+namespace {
+
+struct BatchSetupArgs {
+  double L[GNA_MAX_NBASE];
+  double omega[GNA_MAX_NBASE];
+  double omega_sum;  // sum_b omega_b (left to right)
+  int nbase;
+  int order;
+  int64_t nbins;
+  int64_t npoints;
+};
+
+// Workspace layout of the batch path (all offsets 16-byte aligned), see
+// gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
+// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp].
+struct BatchWs {
+  double2* coef;
+  double* c0;
+  double* invE;
+  double* hw;
+  double* partial;
+};
+
+
+
+size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
+  size_t b = align16((size_t)P * nbase * 3 * sizeof(double2));
+  b += align16((size_t)P * sizeof(double));
+  b += 2 * align16((size_t)order * nbins * sizeof(double));
+  if (chi2) b += align16((size_t)P * warps_per_point(nbins) * sizeof(double));
+  return b;
+}
+
+BatchWs batch_ws_carve(void* base, int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
+  char* c = (char*)base;
+  BatchWs w;
+  w.coef = (double2*)c;
+  c += align16((size_t)P * nbase * 3 * sizeof(double2));
+  w.c0 = (double*)c;
+  c += align16((size_t)P * sizeof(double));
+  w.invE = (double*)c;
+  c += align16((size_t)order * nbins * sizeof(double));
+  w.hw = (double*)c;
+  c += align16((size_t)order * nbins * sizeof(double));
+  w.partial = chi2 ? (double*)c : nullptr;
+  return w;
+}
+
+// (a1)+(a2) setup: per-(point, baseline) coefficients and the per-node tables
+//   invE[i][k] = 1 / (c_k + h_k t_i),  hw[i][k] = h_k w_i   (shared by every point).
+__global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
+                                                     const double* __restrict__ th12,
+                                                     const double* __restrict__ th13,
+                                                     const double* __restrict__ d21,
+                                                     const double* __restrict__ d31,
+                                                     const double* __restrict__ edges, BatchWs w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = a.npoints * a.nbase;
+  const int64_t n2 = (int64_t)a.order * a.nbins;
+  if (t < n1) {
+    const int64_t p = t / a.nbase;
+    const int b = (int)(t - p * a.nbase);
+    double s12, c12, s13, c13, w21, w31, w32;
+    sincos(th12[p], &s12, &c12);
+    sincos(th13[p], &s13, &c13);
+    mixing_weights(s12, c12, s13, c13, &w21, &w31, &w32);
+    const double m21 = d21[p], m31 = d31[p];
+    const double m32 = m31 - m21;
+    const double L = a.L[b], om = a.omega[b];
+    double2* c = w.coef + t * 3;
+    c[0] = make_double2(phase_slope(m21, L), om * w21);
+    c[1] = make_double2(phase_slope(m31, L), om * w31);
+    c[2] = make_double2(phase_slope(m32, L), om * w32);
+    if (b == 0) w.c0[p] = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
+  } else if (t < n1 + n2) {
+    const int64_t idx = t - n1;
+    const int i = (int)(idx / a.nbins);
+    const int64_t k = idx - (int64_t)i * a.nbins;
+    const int off = GNA_GL_OFF(a.order);
+    const double e0 = edges[k], e1 = edges[k + 1];
+    const double ctr = 0.5 * (e0 + e1);
+    const double h = 0.5 * (e1 - e0);
+    w.invE[idx] = 1.0 / fma(h, c_gl_t[off + i], ctr);
+    w.hw[idx] = h * c_gl_w[off + i];
+  }
+}
+
+#define GNA_PRAGMA(x) _Pragma(#x)
+#define GNA_UNROLL(n) GNA_PRAGMA(unroll n)
+#ifndef GNA_BATCH_PI
+#define GNA_BATCH_PI 1
+#endif
+#ifndef GNA_BATCH_PI_Q2
+#define GNA_BATCH_PI_Q2 1
+#endif
+#ifndef GNA_BATCH_PI_MAX_TERMS
+#define GNA_BATCH_PI_MAX_TERMS 6
+#endif
+#ifndef GNA_BATCH_PPW_WORK
+#define GNA_BATCH_PPW_WORK 480
+#endif
+#ifndef GNA_BATCH_LDS_PREFETCH
+#define GNA_BATCH_LDS_PREFETCH 0
+#endif
+#ifndef GNA_BATCH_JUNROLL
+#define GNA_BATCH_JUNROLL 1
+#endif
+#ifndef GNA_BATCH_MINB
+#define GNA_BATCH_MINB 1
+#endif
+
+// N GL nodes of one bin at a time: each (kq, omega*w) coefficient load from
+// shared memory feeds N independent sin^2 chains (ILP across nodes).
+template <int N>
+__device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int nterm,
+                                            const double* __restrict__ invE,
+                                            const double* __restrict__ hw, int64_t nbins, int i,
+                                            double c0, double& s) {
+  double iE[N], a[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    iE[n] = invE[(int64_t)(i + n) * nbins];
+    a[n] = 0.0;
+  }
+#if GNA_BATCH_LDS_PREFETCH
+  // the next coefficient pair is loaded before the current one is consumed, so the
+  // LDS latency is not exposed at the top of every iteration
+  double2 cw = sc[0];
+  GNA_UNROLL(GNA_BATCH_JUNROLL)
+  for (int j = 0; j < nterm; ++j) {
+    const double2 cn = sc[j + 1 < nterm ? j + 1 : j];
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+    cw = cn;
+  }
+#else
+  GNA_UNROLL(GNA_BATCH_JUNROLL)
+  for (int j = 0; j < nterm; ++j) {
+    const double2 cw = sc[j];
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+  }
+#endif
+#pragma unroll
+  for (int n = 0; n < N; ++n) s = fma(hw[(int64_t)(i + n) * nbins], c0 - a[n], s);
+}
+
+// remainder of r < N nodes, compile-time group size
+template <int N>
+__device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc, int nterm,
+                                           const double* __restrict__ invE,
+                                           const double* __restrict__ hw, int64_t nbins, int i,
+                                           double c0, double& s) {
+  if constexpr (N > 1) {
+    if (r == N - 1) {
+      batch_nodes<N - 1>(sc, nterm, invE, hw, nbins, i, c0, s);
+      return;
+    }
+    batch_tail<N - 1>(r, sc, nterm, invE, hw, nbins, i, c0, s);
+  }
+}
+
+// Output stores of the batch epilogue (NEXT-4, fused gather):
+//   kOutLocal     plain stores to this GPU's memory;
+//   kOutPeer      plain stores to a peer GPU's memory mapped into this address space
+//                 (symmetric memory over NVLink), system-scope fence at the end;
+//   kOutMulticast multimem.st to an NVLink-SHARP (NVLS) multicast address: one store
+//                 lands in every participating GPU's buffer (all-gather in the epilogue).
+enum { kOutLocal = 0, kOutPeer = 1, kOutMulticast = 2 };
+
+template <int kOut>
+__device__ __forceinline__ void out_store(double* p, double v) {
+  if constexpr (kOut == kOutMulticast)
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  else
+    *p = v;
+}
+
+// (a3)+(a4)+(a5) main pass.  Block = (point p, kWarps x 32 bins); every warp is
+// independent (no block barrier): it copies its point's coefficient row into a
+// warp-private smem slice, then each lane integrates one bin, N GL nodes at a time
+// (N divides the order when possible, so no group runs with reduced ILP).
+template <int kWarps, int N, int kOut>
+__global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
+    int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
+    double* __restrict__ spectra, const double* __restrict__ data) {
+  extern __shared__ double2 s_coef[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pg = blockIdx.x / bpp;                          // point group
+  const int64_t wt = (blockIdx.x - pg * bpp) * kWarps + warp;  // warp tile within a point
+  const int64_t k0 = wt * 32;
+  if (k0 >= nbins) return;  // whole warp
+  double2* sc = s_coef + warp * nterm;
+  const int64_t k = k0 + lane;
+  const bool active = k < nbins;
+  const int64_t kk = active ? k : nbins - 1;
+  const double* __restrict__ invE = w.invE + kk;
+  const double* __restrict__ hw = w.hw + kk;
+  const double D = (data && active) ? data[k] : 1.0;
+  const int64_t wpp = warps_per_point_dev(nbins);
+  // ppw points per warp, same bins: the node tables stay in L1 across points
+  const int64_t pend = min(npoints, (pg + 1) * (int64_t)ppw);
+  for (int64_t p = pg * (int64_t)ppw; p < pend; ++p) {
+    const double2* __restrict__ gc = w.coef + p * nterm;
+    __syncwarp();  // previous point's reads of sc are done
+    for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
+    __syncwarp();
+    const double c0 = w.c0[p];
+    double s = 0.0;
+    int i = 0;
+    for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
+    if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
+    double x2 = 0.0;
+    if (active) {
+      if (spectra) out_store<kOut>(spectra + p * nbins + k, s);
+      const double d = s - D;
+      x2 = d * d / D;
+    }
+    if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
+    }
+  }
+  if constexpr (kOut != kOutLocal) __threadfence_system();  // remote stores before completion
+}
+
+// Small-nbase variant (few terms per node, several points per warp, e.g. cfg4's
+// single-baseline scan): the loops are interchanged so the node group is outer and the
+// warp's points inner — 1/E and h*w of a node group are loaded once for all ppw points
+// instead of once per point.  Per point the node sums are accumulated in the same order
+// as k_oscprob_batch, so the results are bitwise identical.
+constexpr int kMaxPPW = 16;
+
+template <int N, int kOut>
+__global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
+    int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
+    double* __restrict__ spectra, const double* __restrict__ data) {
+  extern __shared__ double2 s_dyn[];
+  double2* sc = s_dyn;                                          // [ppw][nterm]
+  double* s_acc = reinterpret_cast<double*>(s_dyn + ppw * nterm);  // [ppw][32]
+  double* s_c0 = s_acc + ppw * 32;                               // [ppw]
+  const int lane = threadIdx.x & 31;
+  const int64_t pg = blockIdx.x / bpp;
+  const int64_t wt = blockIdx.x - pg * bpp;
+  const int64_t k0 = wt * 32;
+  if (k0 >= nbins) return;
+  const int64_t p0 = pg * (int64_t)ppw;
+  const int np = (int)min((int64_t)ppw, npoints - p0);
+  for (int j = lane; j < np * nterm; j += 32) sc[j] = w.coef[p0 * nterm + j];
+  for (int j = lane; j < np; j += 32) s_c0[j] = w.c0[p0 + j];
+  for (int q = 0; q < np; ++q) s_acc[q * 32 + lane] = 0.0;
+  __syncwarp();
+  const int64_t k = k0 + lane;
+  const bool active = k < nbins;
+  const int64_t kk = active ? k : nbins - 1;
+  const double* __restrict__ invE = w.invE + kk;
+  const double* __restrict__ hw = w.hw + kk;
+  for (int i = 0; i < order; i += N) {
+    const int nn = min(N, order - i);
+    double iE[N], hv[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      iE[n] = n < nn ? invE[(int64_t)(i + n) * nbins] : 1.0;
+      hv[n] = n < nn ? hw[(int64_t)(i + n) * nbins] : 0.0;
+    }
+    int q = 0;
+#if GNA_BATCH_PI_Q2
+    // two points at a time: 2N independent sin^2 chains per coefficient step
+    for (; q + 1 < np; q += 2) {
+      const double2* __restrict__ cq = sc + q * nterm;
+      const double2* __restrict__ cr = cq + nterm;
+      double a[N], b[N];
+#pragma unroll
+      for (int n = 0; n < N; ++n) a[n] = b[n] = 0.0;
+      for (int j = 0; j < nterm; ++j) {
+        const double2 cw = cq[j], cv = cr[j];
+#pragma unroll
+        for (int n = 0; n < N; ++n) {
+          a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+          b[n] = fma(cv.y, gna::sin2c(cv.x, iE[n]), b[n]);
+        }
+      }
+      const double c0a = s_c0[q], c0b = s_c0[q + 1];
+      double sa = s_acc[q * 32 + lane], sb = s_acc[(q + 1) * 32 + lane];
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < nn) {
+          sa = fma(hv[n], c0a - a[n], sa);
+          sb = fma(hv[n], c0b - b[n], sb);
+        }
+      s_acc[q * 32 + lane] = sa;
+      s_acc[(q + 1) * 32 + lane] = sb;
+    }
+#endif
+    for (; q < np; ++q) {
+      const double2* __restrict__ cq = sc + q * nterm;
+      double a[N];
+#pragma unroll
+      for (int n = 0; n < N; ++n) a[n] = 0.0;
+      for (int j = 0; j < nterm; ++j) {
+        const double2 cw = cq[j];
+#pragma unroll
+        for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+      }
+      const double c0 = s_c0[q];
+      double sv = s_acc[q * 32 + lane];
+#pragma unroll
+      for (int n = 0; n < N; ++n)
+        if (n < nn) sv = fma(hv[n], c0 - a[n], sv);
+      s_acc[q * 32 + lane] = sv;
+    }
+  }
+  const double D = (data && active) ? data[k] : 1.0;
+  const int64_t wpp = warps_per_point_dev(nbins);
+  for (int q = 0; q < np; ++q) {
+    const int64_t p = p0 + q;
+    const double sv = s_acc[q * 32 + lane];
+    double x2 = 0.0;
+    if (active) {
+      if (spectra) out_store<kOut>(spectra + p * nbins + k, sv);
+      const double d = sv - D;
+      x2 = d * d / D;
+    }
+    if (w.partial) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
+    }
+  }
+  if constexpr (kOut != kOutLocal) __threadfence_system();
+}
+
+// chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
+// in order, then a fixed xor tree (deterministic, independent of scheduling).
+template <int kOut>
+__global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
+                                                                int64_t npoints, int64_t wpp,
+                                                                double* __restrict__ chi2) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= npoints) return;
+  const double* q = partial + p * wpp;
+  double s = 0.0;
+  for (int64_t j = lane; j < wpp; j += 32) s += q[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out_store<kOut>(chi2 + p, s);
+  if constexpr (kOut != kOutLocal) __threadfence_system();
+}
+
+}  // namespace

@@ -1,0 +1,66 @@
+// k_fit.cuh — NEXT-4b on-GPU chi^2 pattern-search kernels
+// Part of libgna_b200.so: included once, from gna_b200.cu (single translation unit).
+#pragma once
+#include "gna_common.cuh"
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// NEXT-4 (second part): a chi^2 minimiser that stays on the GPU (the fit of P:446-451).
+// Deterministic compass/pattern search over (theta12, theta13, dm2_21, dm2_31): every
+// iteration evaluates the 3^4 = 81 points centre + step * {-1, 0, +1}^4 with the batch
+// kernels (chi^2 only), takes the argmin (lowest index on ties), moves the centre there,
+// or halves the steps if the centre is already best.  The whole loop is stream-ordered
+// (no host round trip), so it can be captured in one CUDA graph.
+constexpr int kFitDim = 4;
+constexpr int kFitCand = 81;  // 3^4
+
+// state = {centre[4], step[4]} (device, fp64)
+__global__ void __launch_bounds__(128) k_fit_candidates(const double* __restrict__ state,
+                                                        double* __restrict__ cand) {
+  const int c = threadIdx.x;
+  if (c >= kFitCand) return;
+  int code = c;
+#pragma unroll
+  for (int d = 0; d < kFitDim; ++d) {
+    const int o = code % 3 - 1;  // -1, 0, +1 ; candidate 40 is the centre
+    code /= 3;
+    cand[d * kFitCand + c] = fma((double)o, state[kFitDim + d], state[d]);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_fit_update(double* __restrict__ state,
+                                                    const double* __restrict__ cand,
+                                                    const double* __restrict__ chi2,
+                                                    double* __restrict__ hist, int iter) {
+  __shared__ double s_v[128];
+  __shared__ int s_i[128];
+  const int t = threadIdx.x;
+  s_v[t] = t < kFitCand ? chi2[t] : INFINITY;
+  s_i[t] = t;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {  // argmin, ties -> lowest index (deterministic)
+    if (t < o) {
+      const double a = s_v[t], b = s_v[t + o];
+      if (b < a || (b == a && s_i[t + o] < s_i[t])) {
+        s_v[t] = b;
+        s_i[t] = s_i[t + o];
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const int best = s_i[0];
+    const int centre = kFitCand / 2;
+    if (best == centre || !(s_v[0] < chi2[centre])) {
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[kFitDim + d] *= 0.5;
+    } else {
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[d] = cand[d * kFitCand + best];
+    }
+    if (hist) hist[iter] = fmin(s_v[0], chi2[centre]);
+  }
+}
+
+}  // namespace

@@ -1,0 +1,199 @@
+// k_scan.cuh — NEXT-1 separable grid-scan kernels
+// Part of libgna_b200.so: included once, from gna_b200.cu (single translation unit).
+#pragma once
+#include "k_batch.cuh"
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// NEXT-1: separable grid scan ("computed only once ... re-computed
+// only if any of the variables or inputs it depends on were modified", P:641-642 one
+// transformation per formula item).  The mixing weights enter P_ee only linearly, so for a
+// grid {mixing points a} x {mass points c} the binned sin^2 sums depend on c alone:
+//   G[c][ij][k] = sum_b omega_b h_k sum_i w_i sin^2(Delta_ij(c, b, E_ki)),
+//   H[k]        = Omega h_k sum_i w_i,
+//   T[c*nmix+a][k] = H[k] - sum_ij w_ij(a) G[c][ij][k]      (a rank-3 update per point).
+// Stage A costs nmass x nbase x 3 x nbins x order sin^2 (FP64); stage B is bound by writing
+// the spectra to HBM.
+struct ScanArgs {
+  double L[GNA_MAX_NBASE];
+  double omega[GNA_MAX_NBASE];
+  double omega_sum;
+  int nbase;
+  int order;
+  int64_t nbins;
+  int64_t nmix;
+  int64_t nmass;
+};
+
+struct ScanWs {
+  double* G;     // [nmass][3][nbins]
+  double* H;     // [nbins]
+  double* invD;  // [nbins]  1 / data (chi2 only)
+  double* wmix;  // [nmix][4]  (w21, w31, w32, 0)
+};
+
+size_t scan_ws_bytes(int64_t nmix, int64_t nmass, int64_t nbins) {
+  size_t b = align32((size_t)nmass * 3 * nbins * sizeof(double));
+  b += 2 * align32((size_t)nbins * sizeof(double));
+  b += align32((size_t)nmix * 4 * sizeof(double));
+  return b;
+}
+
+ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
+  char* c = (char*)base;
+  ScanWs w;
+  w.G = (double*)c;
+  c += align32((size_t)nmass * 3 * nbins * sizeof(double));
+  w.H = (double*)c;
+  c += align32((size_t)nbins * sizeof(double));
+  w.invD = (double*)c;
+  c += align32((size_t)nbins * sizeof(double));
+  w.wmix = (double*)c;
+  return w;
+}
+
+// stage A: thread per (mass point c, bin k): the three pairs share each node's
+// reciprocal and run as three independent sin^2 chains (two nodes per iteration:
+// six chains) -> G[c][*][k]; threads with c == 0 also write H[k] and 1/D[k]; extra
+// threads compute the mixing weights of each mixing point.
+__global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
+                                                    const double* __restrict__ th13,
+                                                    const double* __restrict__ d21,
+                                                    const double* __restrict__ d31,
+                                                    const double* __restrict__ edges,
+                                                    const double* __restrict__ data, ScanWs w) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = a.nmass * a.nbins;
+  if (t < n1) {
+    const int64_t c = t / a.nbins;
+    const int64_t k = t - c * a.nbins;
+    const int off = GNA_GL_OFF(a.order);
+    const double e0 = edges[k], e1 = edges[k + 1];
+    const double ctr = 0.5 * (e0 + e1);
+    const double h = 0.5 * (e1 - e0);
+    double wsum = 0.0;
+    for (int i = 0; i < a.order; ++i) wsum += c_gl_w[off + i];
+    const double m21 = d21[c], m31 = d31[c];
+    const double m32 = m31 - m21;
+    double G0 = 0.0, G1 = 0.0, G2 = 0.0;
+    for (int b = 0; b < a.nbase; ++b) {
+      const double k0 = phase_slope(m21, a.L[b]);
+      const double k1 = phase_slope(m31, a.L[b]);
+      const double k2 = phase_slope(m32, a.L[b]);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll 2
+      for (int i = 0; i < a.order; ++i) {
+        const double invE = gna::rcp(fma(h, c_gl_t[off + i], ctr));
+        const double wi = c_gl_w[off + i];
+        s0 = fma(wi, gna::sin2c(k0, invE), s0);
+        s1 = fma(wi, gna::sin2c(k1, invE), s1);
+        s2 = fma(wi, gna::sin2c(k2, invE), s2);
+      }
+      // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
+      const double ob = a.omega[b] * h;
+      G0 = fma(ob, fma(0.5, wsum, s0), G0);
+      G1 = fma(ob, fma(0.5, wsum, s1), G1);
+      G2 = fma(ob, fma(0.5, wsum, s2), G2);
+    }
+    double* g = w.G + (c * 3) * a.nbins + k;
+    g[0] = G0;
+    g[a.nbins] = G1;
+    g[2 * a.nbins] = G2;
+    if (c == 0) {
+      w.H[k] = a.omega_sum * h * wsum;
+      if (data) w.invD[k] = 1.0 / data[k];
+    }
+  } else if (t < n1 + a.nmix) {
+    const int64_t mm = t - n1;
+    double s12, c12, s13, c13;
+    sincos(th12[mm], &s12, &c12);
+    sincos(th13[mm], &s13, &c13);
+    double* wm = w.wmix + 4 * mm;
+    mixing_weights(s12, c12, s13, c13, &wm[0], &wm[1], &wm[2]);
+    wm[3] = 0.0;
+  }
+}
+
+// stage B: block = (mass point c, chunk of kScanA (4) mixing points).  Each thread loads
+// G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
+// (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
+// point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
+#ifndef GNA_SCAN_A
+#define GNA_SCAN_A 4
+#endif
+#ifndef GNA_SCAN_THREADS
+#define GNA_SCAN_THREADS 128
+#endif
+constexpr int kScanThreads = GNA_SCAN_THREADS;
+constexpr int kScanA = GNA_SCAN_A;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int64_t nbins,
+                                                              int64_t nchunk, ScanWs w,
+                                                              double* __restrict__ spectra,
+                                                              const double* __restrict__ data,
+                                                              double* __restrict__ chi2) {
+  __shared__ double s_x2[kScanA][kScanThreads / 32];
+  const int64_t c = blockIdx.x / nchunk;
+  const int64_t a0 = (blockIdx.x - c * nchunk) * kScanA;
+  const int na = (int)min((int64_t)kScanA, nmix - a0);
+  double w0[kScanA], w1[kScanA], w2[kScanA], x2[kScanA];
+#pragma unroll
+  for (int j = 0; j < kScanA; ++j) {
+    const int64_t aj = a0 + (j < na ? j : 0);
+    const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * aj);
+    w0[j] = wm.x;
+    w1[j] = wm.y;
+    w2[j] = wm.z;
+    x2[j] = 0.0;
+  }
+  const double* __restrict__ g0 = w.G + (c * 3) * nbins;
+  const double* __restrict__ g1 = g0 + nbins;
+  const double* __restrict__ g2 = g1 + nbins;
+  double* __restrict__ out = spectra ? spectra + (c * nmix + a0) * nbins : nullptr;
+  // software-pipelined: the 6 loads of bin k + kScanThreads are issued before bin k's
+  // outputs are computed, so one L2 round trip is always in flight per thread
+  int64_t k = threadIdx.x;
+  double G0 = 0, G1 = 0, G2 = 0, H = 0, D = 0, iD = 0;
+  if (k < nbins) {
+    G0 = g0[k], G1 = g1[k], G2 = g2[k], H = w.H[k];
+    if (chi2) D = data[k], iD = w.invD[k];
+  }
+  for (; k < nbins; k += kScanThreads) {
+    const int64_t kn = k + kScanThreads;
+    double nG0 = 0, nG1 = 0, nG2 = 0, nH = 0, nD = 0, niD = 0;
+    if (kn < nbins) {
+      nG0 = g0[kn], nG1 = g1[kn], nG2 = g2[kn], nH = w.H[kn];
+      if (chi2) nD = data[kn], niD = w.invD[kn];
+    }
+#pragma unroll
+    for (int j = 0; j < kScanA; ++j) {
+      if (j < na) {
+        const double T = H - fma(w0[j], G0, fma(w1[j], G1, w2[j] * G2));
+        if (out) __stcs(out + (int64_t)j * nbins + k, T);
+        const double d = T - D;
+        x2[j] = fma(d * d, iD, x2[j]);
+      }
+    }
+    G0 = nG0, G1 = nG1, G2 = nG2, H = nH, D = nD, iD = niD;
+  }
+  if (chi2) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < kScanA; ++j) {
+      double v = x2[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s_x2[j][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < na) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < kScanThreads / 32; ++i) t += s_x2[threadIdx.x][i];
+      chi2[c * nmix + a0 + threadIdx.x] = t;
+    }
+  }
+}
+
+}  // namespace
