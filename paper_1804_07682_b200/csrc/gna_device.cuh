@@ -121,4 +121,41 @@ __device__ __forceinline__ double pab_inv(const PabCoef& c, double invE) {
 __device__ __forceinline__ double prob_inv(const PeeCoef& c, double invE) { return pee_inv(c, invE); }
 __device__ __forceinline__ double prob_inv(const PabCoef& c, double invE) { return pab_inv(c, invE); }
 
+// H energies at once, term-major: every coefficient feeds H independent chains (ILP = H).
+// The term loop is deliberately not unrolled: one basic block per term keeps ptxas from
+// serialising the H chains to save registers (it does so in fully unrolled straight-line
+// code); the coefficient is picked with selects, not a dynamically indexed parameter.
+template <int H>
+__device__ __forceinline__ void prob_inv_n(const PeeCoef& c, const double (&iE)[H], double (&P)[H]) {
+  double acc[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) acc[i] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    const double kq = j == 0 ? c.kq[0] : (j == 1 ? c.kq[1] : c.kq[2]);
+    const double w = j == 0 ? c.w[0] : (j == 1 ? c.w[1] : c.w[2]);
+#pragma unroll
+    for (int i = 0; i < H; ++i) acc[i] = fma(w, sin2c(kq, iE[i]), acc[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) P[i] = c.c0 - acc[i];
+}
+
+template <int H>
+__device__ __forceinline__ void prob_inv_n(const PabCoef& c, const double (&iE)[H], double (&P)[H]) {
+  double acc[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) acc[i] = 0.0;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    const double kq = j == 0 ? c.kq[0] : (j == 1 ? c.kq[1] : c.kq[2]);
+    const double a = j == 0 ? c.a[0] : (j == 1 ? c.a[1] : c.a[2]);
+    const double b = j == 0 ? c.b[0] : (j == 1 ? c.b[1] : c.b[2]);
+#pragma unroll
+    for (int i = 0; i < H; ++i) acc[i] += sin2_sin_c(kq, iE[i], a, b);
+  }
+#pragma unroll
+  for (int i = 0; i < H; ++i) P[i] = c.c0 + acc[i];
+}
+
 }  // namespace gna

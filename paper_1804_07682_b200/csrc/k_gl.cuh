@@ -13,10 +13,13 @@ namespace {
 // halves are combined with one shuffle.  The whole grid is resident in one wave, so
 // the bin edges' DRAM latency is paid once.  GL nodes/weights are read per lane
 // from a global (L1) copy of the table.
+#ifndef GNA_GL_MINB
+#define GNA_GL_MINB 8
+#endif
 constexpr int kGLLaneThreads = 128;
 
 template <int kOrder, class Coef>
-__global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(Coef c,
+__global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Coef c,
                                                                  const double* __restrict__ edges,
                                                                  int64_t nbins,
                                                                  double* __restrict__ bins) {
@@ -30,14 +33,17 @@ __global__ void __launch_bounds__(kGLLaneThreads) k_gl_integrate(Coef c,
   const double e0 = edges[kk], e1 = edges[kk + 1];
   const double ctr = 0.5 * (e0 + e1);
   const double h = 0.5 * (e1 - e0);
-  double pv[H];
+  double iE[H], pv[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int node = half * H + i < kOrder ? half * H + i : kOrder - 1;
+    iE[i] = gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr));
+  }
+  gna::prob_inv_n<H>(c, iE, pv);
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int node = half * H + i;
-    pv[i] = 0.0;
-    if (node < kOrder)
-      pv[i] = __ldg(&g_gl_w[off + node]) *
-              gna::prob_inv(c, gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr)));
+    pv[i] = node < kOrder ? __ldg(&g_gl_w[off + node]) * pv[i] : 0.0;
   }
   double s = 0.0;
 #pragma unroll
