@@ -251,17 +251,23 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
                : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut>
                                   : k_oscprob_batch_pi<4, kOut>;
     kpi<<<(unsigned)(ng * bpp), 32, smem_pi, s>>>(nterm, order, nbins, pts->npoints, bpp,
-                                                  (int)ppw, w, spectra, chi2 ? data : nullptr,
-                                                  chi2);
+                                                  (int)ppw, w, spectra, chi2 ? data : nullptr);
   } else {
     kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
-        nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr,
-        chi2);
+        nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
-  // chi2 is folded by the last warp of each point inside the main kernel (no reduce launch)
+  if (chi2) {
+    const int64_t threads = pts->npoints * 32;
+    const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
+    k_chi2_reduce<kOut><<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints,
+                                                        warps_per_point(nbins), chi2);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   return GNA_OK;
 }
 

@@ -35,7 +35,7 @@ constexpr int kEvalThreads = 256;
 #define GNA_BATCH_WARPS 1
 #endif
 constexpr int kBatchWarps = GNA_BATCH_WARPS;
-
+constexpr int kReduceThreads = 128;
 
 __device__ __forceinline__ int64_t warps_per_point_dev(int64_t nbins) { return (nbins + 31) / 32; }
 

@@ -1,4 +1,4 @@
-// k_batch.cuh — (a1)-(a5) batch kernels: setup, per-point / points-inner main pass with the chi2 fold
+// k_batch.cuh — (a1)-(a5) batch kernels: setup, per-point / points-inner main pass, chi2 reduce
 // Part of libgna_b200.so: included once, from gna_b200.cu (single translation unit).
 #pragma once
 #include "gna_common.cuh"
@@ -17,14 +17,13 @@ struct BatchSetupArgs {
 
 // Workspace layout of the batch path (all offsets 16-byte aligned), see
 // gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
-// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp], count [P] (u32).
+// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp].
 struct BatchWs {
   double2* coef;
   double* c0;
   double* invE;
   double* hw;
   double* partial;
-  unsigned* count;  // warps of point p done so far (the last one folds the partials)
 };
 
 
@@ -34,7 +33,6 @@ size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2)
   b += align16((size_t)P * sizeof(double));
   b += 2 * align16((size_t)order * nbins * sizeof(double));
   if (chi2) b += align16((size_t)P * warps_per_point(nbins) * sizeof(double));
-  if (chi2) b += align16((size_t)P * sizeof(unsigned));
   return b;
 }
 
@@ -50,52 +48,7 @@ BatchWs batch_ws_carve(void* base, int64_t P, int nbase, int64_t nbins, int orde
   w.hw = (double*)c;
   c += align16((size_t)order * nbins * sizeof(double));
   w.partial = chi2 ? (double*)c : nullptr;
-  if (chi2) c += align16((size_t)P * warps_per_point(nbins) * sizeof(double));
-  w.count = chi2 ? (unsigned*)c : nullptr;
   return w;
-}
-
-// Output stores of the batch epilogue (NEXT-4, fused gather):
-//   kOutLocal     plain stores to this GPU's memory;
-//   kOutPeer      plain stores to a peer GPU's memory mapped into this address space
-//                 (symmetric memory over NVLink), system-scope fence at the end;
-//   kOutMulticast multimem.st to an NVLink-SHARP (NVLS) multicast address: one store
-//                 lands in every participating GPU's buffer (all-gather in the epilogue).
-enum { kOutLocal = 0, kOutPeer = 1, kOutMulticast = 2 };
-
-template <int kOut>
-__device__ __forceinline__ void out_store(double* p, double v) {
-  if constexpr (kOut == kOutMulticast)
-    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-  else
-    *p = v;
-}
-
-// chi2 epilogue of one warp tile (lane 0 holds the tile's partial): the partial is
-// published, and the warp that completes point p (atomic count) folds the point's
-// partials in a fixed order (lane-strided, then a fixed xor tree) — deterministic
-// whichever warp finishes last, and no separate reduce launch.
-template <int kOut>
-__device__ __forceinline__ void chi2_tile_done(const BatchWs& w, int64_t p, int64_t wt,
-                                               int64_t wpp, double x2, double* chi2, int lane) {
-  unsigned last = 0;
-  if (lane == 0) {
-    w.partial[p * wpp + wt] = x2;
-    __threadfence();  // release the partial before counting this tile
-    last = atomicAdd(&w.count[p], 1u) == (unsigned)(wpp - 1);
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();  // acquire the other tiles' partials
-  const volatile double* q = w.partial + p * wpp;
-  double s = 0.0;
-  for (int64_t j = lane; j < wpp; j += 32) s += q[j];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) {
-    out_store<kOut>(chi2 + p, s);
-    w.count[p] = 0u;  // ready for the next call (graph replays reuse the workspace)
-  }
 }
 
 // (a1)+(a2) setup: per-(point, baseline) coefficients and the per-node tables
@@ -123,10 +76,7 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
     c[0] = make_double2(phase_slope(m21, L), om * w21);
     c[1] = make_double2(phase_slope(m31, L), om * w31);
     c[2] = make_double2(phase_slope(m32, L), om * w32);
-    if (b == 0) {
-      w.c0[p] = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
-      if (w.count) w.count[p] = 0u;
-    }
+    if (b == 0) w.c0[p] = a.omega_sum * (1.0 - 0.5 * ((w21 + w31) + w32));
   } else if (t < n1 + n2) {
     const int64_t idx = t - n1;
     const int i = (int)(idx / a.nbins);
@@ -215,6 +165,22 @@ __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc
   }
 }
 
+// Output stores of the batch epilogue (NEXT-4, fused gather):
+//   kOutLocal     plain stores to this GPU's memory;
+//   kOutPeer      plain stores to a peer GPU's memory mapped into this address space
+//                 (symmetric memory over NVLink), system-scope fence at the end;
+//   kOutMulticast multimem.st to an NVLink-SHARP (NVLS) multicast address: one store
+//                 lands in every participating GPU's buffer (all-gather in the epilogue).
+enum { kOutLocal = 0, kOutPeer = 1, kOutMulticast = 2 };
+
+template <int kOut>
+__device__ __forceinline__ void out_store(double* p, double v) {
+  if constexpr (kOut == kOutMulticast)
+    asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  else
+    *p = v;
+}
+
 // (a3)+(a4)+(a5) main pass.  Block = (point p, kWarps x 32 bins); every warp is
 // independent (no block barrier): it copies its point's coefficient row into a
 // warp-private smem slice, then each lane integrates one bin, N GL nodes at a time
@@ -222,7 +188,7 @@ __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc
 template <int kWarps, int N, int kOut>
 __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
-    double* __restrict__ spectra, const double* __restrict__ data, double* __restrict__ chi2) {
+    double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double2 s_coef[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pg = blockIdx.x / bpp;                          // point group
@@ -258,7 +224,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-      chi2_tile_done<kOut>(w, p, wt, wpp, x2, chi2, lane);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
     }
   }
   if constexpr (kOut != kOutLocal) __threadfence_system();  // remote stores before completion
@@ -274,7 +240,7 @@ constexpr int kMaxPPW = 16;
 template <int N, int kOut>
 __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
     int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
-    double* __restrict__ spectra, const double* __restrict__ data, double* __restrict__ chi2) {
+    double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double2 s_dyn[];
   double2* sc = s_dyn;                                          // [ppw][nterm]
   double* s_acc = reinterpret_cast<double*>(s_dyn + ppw * nterm);  // [ppw][32]
@@ -364,11 +330,28 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
     if (w.partial) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
-      chi2_tile_done<kOut>(w, p, wt, wpp, x2, chi2, lane);
+      if (lane == 0) w.partial[p * wpp + wt] = x2;
     }
   }
   if constexpr (kOut != kOutLocal) __threadfence_system();
 }
 
+// chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
+// in order, then a fixed xor tree (deterministic, independent of scheduling).
+template <int kOut>
+__global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
+                                                                int64_t npoints, int64_t wpp,
+                                                                double* __restrict__ chi2) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= npoints) return;
+  const double* q = partial + p * wpp;
+  double s = 0.0;
+  for (int64_t j = lane; j < wpp; j += 32) s += q[j];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out_store<kOut>(chi2 + p, s);
+  if constexpr (kOut != kOutLocal) __threadfence_system();
+}
 
 }  // namespace
