@@ -384,9 +384,16 @@ def main():
         gather_mode = "none" if world == 1 else "nccl"
         if world > 1 and args.gather in ("auto", "fused"):
             # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
-            # validated bitwise against the NCCL gather before it is used
+            # every rank must have built it before any rank runs it, and it is validated
+            # bitwise against the NCCL gather before it is used
+            fg, err = None, ""
             try:
                 fg = gdist.FusedGather(P, nb, dev)
+            except Exception as exc:  # noqa: BLE001 — reported in config.gather
+                err = str(exc).splitlines()[0][:120] if str(exc) else type(exc).__name__
+            built = torch.tensor([1.0 if fg is not None else 0.0], device=dev)
+            dist.all_reduce(built, op=dist.ReduceOp.MIN)
+            if float(built) == 1.0:
                 sp_ptr, x2_ptr, fflags = fg.out_ptrs()
 
                 def step_fused():
@@ -410,8 +417,9 @@ def main():
                 else:
                     gather_mode = "nccl (fused epilogue failed bitwise validation)"
                 del s_ref, x_ref
-            except Exception as exc:  # noqa: BLE001 — fall back to the NCCL path, and say so
-                gather_mode = "nccl (fused epilogue unavailable: %s)" % str(exc).splitlines()[0][:120]
+            else:
+                gather_mode = "nccl (fused epilogue unavailable on some rank%s)" % (
+                    ": " + err if err else "")
             kern_ev.clear()
 
         units_per_rank = (hi - lo) * L.size * nb * c["order"]

@@ -209,9 +209,10 @@ class FusedGather:
         flags = GNA_OUT_MULTICAST if self.multicast else GNA_OUT_PEER
         return sb + self.lo * self.nbins * 8, cb + self.lo * 8, flags
 
-    def barrier(self):
-        """Device-side barrier on the current stream: every rank's remote writes are done."""
-        self.h_spec.barrier(channel=0)
+    def barrier(self, timeout_ms: int = 60_000):
+        """Device-side barrier on the current stream: every rank's remote writes are done
+        (finite timeout, so a missing rank is an error rather than a hang)."""
+        self.h_spec.barrier(channel=0, timeout_ms=timeout_ms)
 
     def result(self):
         """The gathered (spectra, chi2) as local tensors (all ranks with multicast, rank 0 else)."""
