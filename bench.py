@@ -658,6 +658,16 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(c, "cfg5" if args.workload == "cfg5fit" else
                                             args.workload, args.cpu_seconds)
+        # Table-1-style ratios: CPU time / GPU time for the same work
+        cpu_v = line["cpu_baseline"]["value"]
+        e2e_v = (line.get("e2e") or {}).get("value")
+        line["table1_context"] = {
+            "cpu_over_gpu_compute_only": value / cpu_v,
+            "cpu_over_gpu_incl_transfer": (e2e_v / cpu_v) if e2e_v else None,
+            "paper": {"cpu_over_gpu_compute_only": {"1e4": 20.90, "1e6": 26.46},
+                      "cpu_over_gpu_incl_transfer": {"1e4": 0.017, "1e6": 1.39},
+                      "hardware": "Intel Core i7-6700HQ vs NVIDIA GeForce GTX 970M, fp64",
+                      "source": "PAPER.md Table 1 (P:658-689); context only"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
