@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--lib", default=None, help="alternative libgna_b200.so (tuning variants)")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only to exercise the N>1 code path on "
+                         "one GPU, with GNA_BENCH_SAME_DEVICE=1; not for measurements)")
     ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "fused"],
                     help="N>1 exchange: fused kernel-epilogue stores (validated) or NCCL all-gather")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -345,11 +348,18 @@ def main():
     import paper_1804_07682_b200 as gna
     from paper_1804_07682_b200 import dist as gdist
 
+    if os.environ.get("GNA_BENCH_SAME_DEVICE") == "1":
+        local = 0  # code-path test: every rank on GPU 0 (independent kernels, no device spin)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+            if args.gather != "nccl":
+                args.gather = "nccl"  # the fused epilogue needs one GPU per rank
     gna.load(args.lib)
     c = workload(args.workload)
     f64 = dict(dtype=torch.float64, device=dev)
@@ -521,7 +531,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            _barrier(dist, args, local)
 
     # ---------------- warm-up
     for _ in range(max(args.warmup, 3)):
@@ -671,8 +681,15 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier(device_ids=[local])
+        _barrier(dist, args, local)
         dist.destroy_process_group()
+
+
+def _barrier(dist, args, local):
+    if args.backend == "nccl":
+        dist.barrier(device_ids=[local])
+    else:
+        dist.barrier()
 
 
 def _ncu_traffic(workload: str):
@@ -772,7 +789,7 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
     one()
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier(device_ids=[local])
+        _barrier(dist, args, local)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -790,7 +807,7 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
         one_spectra()
         torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            _barrier(dist, args, local)
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record()
