@@ -392,6 +392,7 @@ def main():
             sb.step(compute, comm_stream=comm)
 
         gather_mode = "none" if world == 1 else "nccl"
+        fused_fg = None
         if world > 1 and args.gather in ("auto", "fused"):
             # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
             # every rank must have built it before any rank runs it, and it is validated
@@ -423,6 +424,7 @@ def main():
                 dist.all_reduce(ok, op=dist.ReduceOp.MIN)
                 if float(ok) == 1.0:
                     step = step_fused  # noqa: F811
+                    fused_fg = fg
                     gather_mode = "fused-epilogue-" + ("multicast" if fg.multicast else "peer-to-root")
                 else:
                     gather_mode = "nccl (fused epilogue failed bitwise validation)"
@@ -657,6 +659,12 @@ def main():
             "cuda_graph": bool(use_graph)}
     if args.workload in ("cfg4", "cfg5"):
         line["config"]["gather"] = gather_mode
+        if world > 1:
+            # the gathered result after the timed steps must equal a single-GPU batch of
+            # all points, bit for bit (checked on rank 0, outside the timed region)
+            line["config"]["gather_verified"] = _verify_gather(
+                args, c, gna, torch, dist, dev, rank, sb, fused_fg if gather_mode.startswith(
+                    "fused") else None)
 
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
     if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu", "cfg5fit"):
@@ -683,6 +691,21 @@ def main():
     if world > 1:
         _barrier(dist, args, local)
         dist.destroy_process_group()
+
+
+def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
+    """Rank 0: gathered spectra/chi2 == one batch over all points on this GPU (bitwise)."""
+    ok = torch.ones(1, device=dev)
+    if rank == 0:
+        f64 = dict(dtype=torch.float64, device=dev)
+        pts = {k: torch.tensor(v, **f64) for k, v in c["points"].items()}
+        sp, x2 = gna.oscprob_batch(pts, c["L_km"], c["omega"], torch.tensor(c["edges"], **f64),
+                                   c["order"], data=torch.tensor(c["data"], **f64))
+        gs, gx = (fg.spectra, fg.chi2) if fg is not None else sb.gathered()
+        ok.fill_(1.0 if (torch.equal(gs, sp) and torch.equal(gx, x2)) else 0.0)
+        del pts, sp, x2
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(float(ok) == 1.0)
 
 
 def _barrier(dist, args, local):
