@@ -391,7 +391,7 @@ def main():
         def step():
             sb.step(compute, comm_stream=comm)
 
-        gather_mode = "none" if world == 1 else "nccl"
+        gather_mode = "none" if world == 1 else "%s all_gather (chunked)" % args.backend
         fused_fg = None
         if world > 1 and args.gather in ("auto", "fused"):
             # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
