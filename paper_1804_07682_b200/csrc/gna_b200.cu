@@ -235,7 +235,8 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (e != cudaSuccess) return cuda_fail(e);
 
   const int nterm = 3 * nbase;
-  const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
+  const size_t smem = (size_t)kBatchWarps * (GNA_SIN2_FQ ? nterm + (nterm + 3) / 4 : nterm) *
+                      sizeof(double2);
   // node-group size: 5, 4 or 3 when it divides the order, else 4
   auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5, kOut>
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut>

@@ -49,6 +49,32 @@ __device__ __forceinline__ double sin2c(double kq, double invE) {
   return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
 }
 
+// The same term with q = rint(y) found on the FP32 pipe (NEXT: one FP64 instruction fewer):
+// tf = kq_f * invE_f + 1.5*2^23 rounds in fp32; q is read from tf's bits with an integer
+// subtract and rebuilt as an exact double from the bits of 1.5*2^52 + 2^31 + q (one DADD).
+// q can differ from rint(y) by 1 only when y is within |y| * 2^-22 of a half-integer, so
+// |f| <= 0.5 + 2.5e-7 |y|; the minimax stays within 1.3e-16 for |f| <= 0.505, i.e. for
+// |y| <= 2e4.  Valid only for |y| < 2^22 (callers check the bound).
+constexpr double kRoundMagic31 = 6755401588539392.0;  // 1.5 * 2^52 + 2^31
+
+__device__ __forceinline__ double sin2c_fq(double kq, float kqf, double invE, float invEf) {
+  const float tf = fmaf(kqf, invEf, 12582912.0f);  // 1.5 * 2^23
+  const int qi = __float_as_int(tf) - 0x4B400000;
+  const double q = __hiloint2double(0x43380000, qi + (int)0x80000000) - kRoundMagic31;
+  const double f = fma(kq, invE, -q);
+  const double u = f * f;
+  double p = fma(u, c_sin2[8], c_sin2[7]);
+  p = fma(p, u, c_sin2[6]);
+  p = fma(p, u, c_sin2[5]);
+  p = fma(p, u, c_sin2[4]);
+  p = fma(p, u, c_sin2[3]);
+  p = fma(p, u, c_sin2[2]);
+  p = fma(p, u, c_sin2[1]);
+  p = fma(p, u, c_sin2[0]);
+  const int odd = qi << 31;
+  return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
+}
+
 // 1/x for x > 0 (normal): MUFU.RCP64H seed (measured 20 bits, tools/probe_rcp.cu,
 // profiles/r01_probe_rcp.jsonl) + one cubically convergent step r(1 + e + e^2),
 // e = 1 - x r: 3 DFMA, max error 1 ulp (2.2e-16 relative) over 1-10 MeV.

@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI
 #define GNA_BATCH_PI 1
 #endif
+#ifndef GNA_SIN2_FQ
+#define GNA_SIN2_FQ 0
+#endif
 #ifndef GNA_BATCH_PI_Q2
 #define GNA_BATCH_PI_Q2 1
 #endif
@@ -127,7 +130,19 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     iE[n] = invE[(int64_t)(i + n) * nbins];
     a[n] = 0.0;
   }
-#if GNA_BATCH_LDS_PREFETCH
+#if GNA_SIN2_FQ
+  // q on the FP32 pipe: fp32 copies of the coefficients sit right after the double2 row
+  const float* __restrict__ scf = reinterpret_cast<const float*>(sc + nterm);
+  float iEf[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) iEf[n] = __double2float_rn(iE[n]);
+  for (int j = 0; j < nterm; ++j) {
+    const double2 cw = sc[j];
+    const float kf = scf[j];
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c_fq(cw.x, kf, iE[n], iEf[n]), a[n]);
+  }
+#elif GNA_BATCH_LDS_PREFETCH
   // the next coefficient pair is loaded before the current one is consumed, so the
   // LDS latency is not exposed at the top of every iteration
   double2 cw = sc[0];
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const int64_t wt = (blockIdx.x - pg * bpp) * kWarps + warp;  // warp tile within a point
   const int64_t k0 = wt * 32;
   if (k0 >= nbins) return;  // whole warp
-  double2* sc = s_coef + warp * nterm;
+  double2* sc = s_coef + warp * (GNA_SIN2_FQ ? nterm + (nterm + 3) / 4 : nterm);
   const int64_t k = k0 + lane;
   const bool active = k < nbins;
   const int64_t kk = active ? k : nbins - 1;
@@ -208,7 +223,12 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   for (int64_t p = pg * (int64_t)ppw; p < pend; ++p) {
     const double2* __restrict__ gc = w.coef + p * nterm;
     __syncwarp();  // previous point's reads of sc are done
-    for (int j = lane; j < nterm; j += 32) sc[j] = gc[j];
+    for (int j = lane; j < nterm; j += 32) {
+      sc[j] = gc[j];
+#if GNA_SIN2_FQ
+      reinterpret_cast<float*>(sc + nterm)[j] = __double2float_rn(gc[j].x);
+#endif
+    }
     __syncwarp();
     const double c0 = w.c0[p];
     double s = 0.0;

@@ -12,10 +12,9 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "g_m4": dict(GNA_GL_MINB=4),
-    "g_m8": dict(GNA_GL_MINB=8),
-    "g_m12": dict(GNA_GL_MINB=12),
-    "g_m16": dict(GNA_GL_MINB=16),
+    "fq0": dict(GNA_SIN2_FQ=0),
+    "fq1": dict(GNA_SIN2_FQ=1),
+    "fq1n4": dict(GNA_SIN2_FQ=1),
 }
 
 
@@ -28,7 +27,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_gl_integrateILi10EN3gna7PeeCoef.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_batchILi1ELi5ELi0E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
