@@ -12,9 +12,9 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "fq0": dict(GNA_SIN2_FQ=0),
-    "fq1": dict(GNA_SIN2_FQ=1),
-    "fq1n4": dict(GNA_SIN2_FQ=1),
+    "fq1m20": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=20),
+    "fq1m24": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=24),
+    "fq1m16": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=16),
 }
 
 
