@@ -119,6 +119,24 @@ def test_eval_stress_domain_within_conditioning_bound(gna):
         assert np.all(np.abs(P - Pr) <= bound)
 
 
+@pytest.mark.parametrize("L", [1_000.0, 12_000.0])
+def test_eval_huge_phases_within_conditioning_bound(gna, L):
+    """Phases far beyond the reactor domain (atmospheric-like L, E down to 0.1 MeV: |Delta| up
+    to ~3e5 rad): the reduction stays exact (R10), so GPU and oracle differ only by the
+    rounding of the phase itself, bounded by sum_ij |2 Delta_ij| * 8 eps."""
+    g = synth.rng(int(L))
+    for _ in range(4):
+        p = synth.random_params(g)
+        E = g.uniform(0.1, 10.0, 50_000)
+        P = _np(gna.oscprob_eval(p, L, _t(E)))
+        Pr = oracle.prob_array(p, L, E, nthreads=_nt())
+        dm = np.array([p["dm2_21"], p["dm2_31"], p["dm2_31"] - p["dm2_21"]])
+        ph = np.abs(1.26693268 * dm[:, None] * L / (E[None, :] / 1000.0))
+        bound = 1e-15 + np.sum(2 * ph * 8 * EPS, axis=0)
+        assert np.all(np.abs(P - Pr) <= bound)
+        assert np.max(np.abs(P - Pr)) > 0  # (the bound, not luck, is what is being tested)
+
+
 def test_eval_cfg3_full_size_sampled(gna):
     """cfg3: 1e8 energies streamed from HBM, as bench.py launches it; sampled parity."""
     import torch
