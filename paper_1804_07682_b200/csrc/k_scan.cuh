@@ -119,6 +119,9 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
 // G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
 // (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
 // point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
+#ifndef GNA_SCAN_STREAMING_STORES
+#define GNA_SCAN_STREAMING_STORES 1
+#endif
 #ifndef GNA_SCAN_A
 #define GNA_SCAN_A 4
 #endif
@@ -170,7 +173,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
     for (int j = 0; j < kScanA; ++j) {
       if (j < na) {
         const double T = H - fma(w0[j], G0, fma(w1[j], G1, w2[j] * G2));
+#if GNA_SCAN_STREAMING_STORES
         if (out) __stcs(out + (int64_t)j * nbins + k, T);
+#else
+        if (out) out[(int64_t)j * nbins + k] = T;
+#endif
         const double d = T - D;
         x2[j] = fma(d * d, iD, x2[j]);
       }

@@ -12,9 +12,10 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "fq1m20": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=20),
-    "fq1m24": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=24),
-    "fq1m16": dict(GNA_SIN2_FQ=1, GNA_BATCH_MINB=16),
+    "sc_cs": dict(GNA_SCAN_STREAMING_STORES=1),
+    "sc_plain": dict(GNA_SCAN_STREAMING_STORES=0),
+    "sc_plain_a8": dict(GNA_SCAN_STREAMING_STORES=0, GNA_SCAN_A=8),
+    "sc_plain_a2": dict(GNA_SCAN_STREAMING_STORES=0, GNA_SCAN_A=2),
 }
 
 
@@ -27,7 +28,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_batchILi1ELi5ELi0E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_scan_expand.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
