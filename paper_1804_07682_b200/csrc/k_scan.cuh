@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
 // (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
 // point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
 #ifndef GNA_SCAN_STREAMING_STORES
-#define GNA_SCAN_STREAMING_STORES 1
+#define GNA_SCAN_STREAMING_STORES 0
 #endif
 #ifndef GNA_SCAN_A
 #define GNA_SCAN_A 4
