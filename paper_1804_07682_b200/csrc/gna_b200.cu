@@ -220,7 +220,8 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   // keeping >= 16 warps per SM worth of blocks
   const int64_t work = (int64_t)3 * nbase * order;
   const bool small_terms = 3 * nbase <= GNA_BATCH_PI_MAX_TERMS;
-  int64_t ppw = std::max<int64_t>(1, ((small_terms ? GNA_BATCH_PPW_WORK : 240) + work - 1) / work);
+  int64_t ppw = std::max<int64_t>(
+      1, ((small_terms ? GNA_BATCH_PPW_WORK : GNA_BATCH_PPW_WORK_BIG) + work - 1) / work);
   const int64_t min_blocks = (int64_t)sm_count() * 16;
   while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
   const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;

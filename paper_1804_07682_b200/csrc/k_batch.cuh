@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI_MAX_TERMS
 #define GNA_BATCH_PI_MAX_TERMS 6
 #endif
+#ifndef GNA_BATCH_PPW_WORK_BIG
+#define GNA_BATCH_PPW_WORK_BIG 240
+#endif
 #ifndef GNA_BATCH_PPW_WORK
 #define GNA_BATCH_PPW_WORK 480
 #endif
