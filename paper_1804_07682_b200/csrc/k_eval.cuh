@@ -35,6 +35,9 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(Coef c,
 // registers; threads read their double2 pairs from shared memory, compute, and
 // store P with streaming (evict-first) stores.  Full tiles only; the < 1 tile tail
 // is done by block 0 with plain loads.
+#ifndef GNA_EVAL_BULK_STORE
+#define GNA_EVAL_BULK_STORE 0
+#endif
 #ifndef GNA_EVAL_TILE
 #define GNA_EVAL_TILE 1024
 #endif
@@ -76,6 +79,33 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
     const int st = (int)(it % kEvalStages);
     gna::mbar_wait(&s_full[st], (uint32_t)((it / kEvalStages) & 1));
     const int64_t tile = first + it * stride;
+#if GNA_EVAL_BULK_STORE
+    // results overwrite the inputs in the same stage (each thread owns its slots), then one
+    // thread hands the whole 8 KiB tile to the bulk-copy engine (no per-thread stores)
+    double2* buf = reinterpret_cast<double2*>(s_buf[st]);
+#pragma unroll
+    for (int j = threadIdx.x; j < kEvalTile / 2; j += kEvalTmaThreads) {
+      const double2 e = buf[j];
+      double2 r;
+      r.x = gna::prob_inv(c, gna::rcp(e.x));
+      r.y = gna::prob_inv(c, gna::rcp(e.y));
+      buf[j] = r;
+    }
+    gna::fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      gna::bulk_s2g(P + tile * kEvalTile, s_buf[st], kEvalTile * 8);
+      gna::bulk_commit();
+      if (it + kEvalStages < mine) {
+        gna::bulk_wait_read<0>();  // the store has read stage st before it is refilled
+        gna::mbar_expect_tx(&s_full[st], kEvalTile * 8);
+        gna::bulk_g2s(s_buf[st], E + (first + (it + kEvalStages) * stride) * kEvalTile,
+                      kEvalTile * 8, &s_full[st]);
+      }
+    }
+  }
+  if (threadIdx.x == 0) gna::bulk_wait_all();
+#else
     const double2* src = reinterpret_cast<const double2*>(s_buf[st]);
     double2* dst = reinterpret_cast<double2*>(P + tile * kEvalTile);
 #pragma unroll
@@ -93,6 +123,7 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
                     kEvalTile * 8, &s_full[st]);
     }
   }
+#endif
   if (blockIdx.x == 0)
     for (int64_t i = ntiles * kEvalTile + threadIdx.x; i < n; i += kEvalTmaThreads)
       P[i] = gna::prob_inv(c, gna::rcp(E[i]));

@@ -12,9 +12,9 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
-    "big240": dict(GNA_BATCH_PPW_WORK_BIG=240),
-    "big480": dict(GNA_BATCH_PPW_WORK_BIG=480),
-    "big960": dict(GNA_BATCH_PPW_WORK_BIG=960),
+    "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
+    "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
+    "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
 }
 
 
@@ -27,7 +27,7 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_batchILi1ELi5ELi0E.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
+        m = re.search(r"k_oscprob_eval_tmaIN3gna7PeeCoefEEvT_PKdPdl.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
                       cmd_out, re.S)
         print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
