@@ -51,7 +51,8 @@
  *     accurate to the rounding of Delta itself (R7, R9).
  *   Thread safety: stateless and re-entrant for the device entry points;
  *     concurrent calls on disjoint outputs are allowed.  The *_host
- *     entry points serialise on an internal lock per device.
+ *     entry points serialise on an internal lock per device (calls on different
+ *     devices run concurrently).
  */
 #ifndef GNA_B200_H
 #define GNA_B200_H

@@ -132,15 +132,16 @@ int grid_for(int64_t work_items, int threads, int max_blocks) {
   return (int)b;
 }
 
+// SM count of the current device (cached per device; 148 on B200)
 int sm_count() {
-  static std::atomic<int> cached{0};
-  int v = cached.load();
+  static std::atomic<int> cached[128];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 128) return 148;
+  int v = cached[dev].load(std::memory_order_relaxed);
   if (v == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
       v = 148;
-    cached.store(v);
+    cached[dev].store(v, std::memory_order_relaxed);
   }
   return v;
 }
@@ -368,7 +369,7 @@ struct Staging {
   size_t shared_cap = 0;
 };
 
-std::mutex g_stage_mu;
+std::mutex g_stage_mu[128];  // one lock per device: host-buffer calls on different GPUs overlap
 Staging g_stage[128];
 
 int ensure(void** p, size_t* cap, size_t need) {
@@ -463,7 +464,7 @@ int gna_gl_integrate_host(const gna_osc_params* p, double L_km, const double* h_
   if ((rc = check_device())) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_stage_mu);
+  std::lock_guard<std::mutex> lk(g_stage_mu[dev]);
   Staging* S = &g_stage[dev];
   if ((rc = stage_init(S))) return rc;
   if (chunk <= 0) chunk = (int64_t)1 << 20;  // bins per chunk
@@ -651,7 +652,7 @@ int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_
   if ((rc = check_device())) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_stage_mu);
+  std::lock_guard<std::mutex> lk(g_stage_mu[dev]);
   Staging* S = &g_stage[dev];
   if ((rc = stage_init(S))) return rc;
   if (chunk <= 0) chunk = (int64_t)1 << 22;  // 4 Mi elements = 32 MiB per direction
@@ -695,7 +696,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   if ((rc = check_device())) return rc;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_stage_mu);
+  std::lock_guard<std::mutex> lk(g_stage_mu[dev]);
   Staging* S = &g_stage[dev];
   if ((rc = stage_init(S))) return rc;
   const int64_t P = h_pts->npoints;
@@ -765,10 +766,10 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
 }
 
 void gna_release(void) {
-  std::lock_guard<std::mutex> lk(g_stage_mu);
   int cur = 0;
   cudaGetDevice(&cur);
   for (int d = 0; d < 128; ++d) {
+    std::lock_guard<std::mutex> lk(g_stage_mu[d]);
     Staging* S = &g_stage[d];
     if (!S->init && !S->buf[0] && !S->buf[1] && !S->shared) continue;
     cudaSetDevice(d);
