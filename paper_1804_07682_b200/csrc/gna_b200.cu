@@ -16,7 +16,9 @@
 #include <algorithm>
 #include <complex>
 #include <utility>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "../../include/gna_b200.h"
 #include "gna_common.cuh"
@@ -146,6 +148,26 @@ int sm_count() {
   return v;
 }
 
+// resident blocks per SM of a kernel at a dynamic smem size (occupancy API, cached per device)
+[[maybe_unused]] int resident_blocks(const void* kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, size_t>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  const auto key = std::make_tuple(dev, kernel, smem);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess ||
+      n < 1) {
+    cudaGetLastError();
+    n = 1;
+  }
+  cache.emplace(key, n);
+  return n;
+}
+
 // --- validation shared by device and host variants --------------------------
 int validate_eval(const gna_osc_params* p, double L_km, const double* E, int64_t n, const double* P) {
   if (!params_ok(p) || !E || !P || n < 1 || !is_fin(L_km) || L_km < 0) return GNA_EINVAL;
@@ -247,12 +269,39 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
     // several points per warp: node groups outer, points inner (bitwise-identical sums)
     ppw = std::min<int64_t>(ppw, kMaxPPW);
-    const int64_t ng = (pts->npoints + ppw - 1) / ppw;
-    const size_t smem_pi = (size_t)ppw * nterm * sizeof(double2) + (size_t)ppw * 33 * 8;
     auto kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut>
                : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut>
                : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut>
                                   : k_oscprob_batch_pi<4, kOut>;
+#if GNA_BATCH_PI_NT
+    // single baseline (3 terms): term loop unrolled at compile time
+    if (nterm == 3)
+      kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut, 3>
+            : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut, 3>
+            : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut, 3>
+                               : k_oscprob_batch_pi<4, kOut, 3>;
+#endif
+#if GNA_BATCH_PI_TAIL
+    // Few waves (e.g. cfg4: ~8): pick the points per warp in [ppw/2, ppw] that minimises
+    // waves x (ppw + per-block overhead), so the last wave is not mostly idle
+    // (DESIGN.md §6.3).  The grouping never changes a point's result.
+    {
+      const int64_t hi = ppw;
+      double best = 0.0;
+      for (int64_t c = std::max<int64_t>(1, hi / 2); c <= hi; ++c) {
+        const size_t sm_c = (size_t)c * nterm * sizeof(double2) + (size_t)c * 33 * 8;
+        const int64_t slots = (int64_t)sm_count() * resident_blocks((const void*)kpi, 32, sm_c);
+        const int64_t nb = ((pts->npoints + c - 1) / c) * bpp;
+        const double cost = (double)((nb + slots - 1) / slots) * ((double)c + 0.25);
+        if (best == 0.0 || cost <= best) {
+          best = cost;
+          ppw = c;
+        }
+      }
+    }
+#endif
+    const int64_t ng = (pts->npoints + ppw - 1) / ppw;
+    const size_t smem_pi = (size_t)ppw * nterm * sizeof(double2) + (size_t)ppw * 33 * 8;
     kpi<<<(unsigned)(ng * bpp), 32, smem_pi, s>>>(nterm, order, nbins, pts->npoints, bpp,
                                                   (int)ppw, w, spectra, chi2 ? data : nullptr);
   } else {

@@ -119,6 +119,15 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_MINB
 #define GNA_BATCH_MINB 1
 #endif
+#ifndef GNA_BATCH_PI_NT
+#define GNA_BATCH_PI_NT 1
+#endif
+#ifndef GNA_BATCH_PI_TAIL
+#define GNA_BATCH_PI_TAIL 0
+#endif
+#ifndef GNA_BATCH_PI_MINB
+#define GNA_BATCH_PI_MINB GNA_BATCH_MINB
+#endif
 
 // N GL nodes of one bin at a time: each (kq, omega*w) coefficient load from
 // shared memory feeds N independent sin^2 chains (ILP across nodes).
@@ -126,7 +135,7 @@ template <int N>
 __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int nterm,
                                             const double* __restrict__ invE,
                                             const double* __restrict__ hw, int64_t nbins, int i,
-                                            double c0, double& s) {
+                                            double& W, double& A) {
   double iE[N], a[N];
 #pragma unroll
   for (int n = 0; n < N; ++n) {
@@ -165,7 +174,11 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
   }
 #endif
 #pragma unroll
-  for (int n = 0; n < N; ++n) s = fma(hw[(int64_t)(i + n) * nbins], c0 - a[n], s);
+  for (int n = 0; n < N; ++n) {
+    const double h = hw[(int64_t)(i + n) * nbins];
+    W += h;
+    A = fma(h, a[n], A);
+  }
 }
 
 // remainder of r < N nodes, compile-time group size
@@ -173,13 +186,13 @@ template <int N>
 __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc, int nterm,
                                            const double* __restrict__ invE,
                                            const double* __restrict__ hw, int64_t nbins, int i,
-                                           double c0, double& s) {
+                                           double& W, double& A) {
   if constexpr (N > 1) {
     if (r == N - 1) {
-      batch_nodes<N - 1>(sc, nterm, invE, hw, nbins, i, c0, s);
+      batch_nodes<N - 1>(sc, nterm, invE, hw, nbins, i, W, A);
       return;
     }
-    batch_tail<N - 1>(r, sc, nterm, invE, hw, nbins, i, c0, s);
+    batch_tail<N - 1>(r, sc, nterm, invE, hw, nbins, i, W, A);
   }
 }
 
@@ -220,6 +233,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const double* __restrict__ invE = w.invE + kk;
   const double* __restrict__ hw = w.hw + kk;
   const double D = (data && active) ? data[k] : 1.0;
+  const double iD = 1.0 / D;  // once per lane: chi2 terms d^2 / D as d^2 * iD (no per-point divide)
   const int64_t wpp = warps_per_point_dev(nbins);
   // ppw points per warp, same bins: the node tables stay in L1 across points
   const int64_t pend = min(npoints, (pg + 1) * (int64_t)ppw);
@@ -233,16 +247,18 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
 #endif
     }
     __syncwarp();
-    const double c0 = w.c0[p];
-    double s = 0.0;
+    // bin = sum_n h w_n (c0 - a_n) = c0 W - A,  W = sum_n h w_n,  A = sum_n h w_n a_n
+    // (one FP64 op per node instead of two)
+    double W = 0.0, A = 0.0;
     int i = 0;
-    for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, c0, s);
-    if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, c0, s);
+    for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, W, A);
+    if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, W, A);
+    const double s = fma(w.c0[p], W, -A);
     double x2 = 0.0;
     if (active) {
       if (spectra) out_store<kOut>(spectra + p * nbins + k, s);
       const double d = s - D;
-      x2 = d * d / D;
+      x2 = d * d * iD;
     }
     if (w.partial) {  // chi2 requested: fixed xor tree, deterministic
 #pragma unroll
@@ -260,11 +276,12 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
 // as k_oscprob_batch, so the results are bitwise identical.
 constexpr int kMaxPPW = 16;
 
-template <int N, int kOut>
-__global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
-    int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
+template <int N, int kOut, int NT = 0>
+__global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
+    int nterm_rt, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double2 s_dyn[];
+  const int nterm = NT ? NT : nterm_rt;  // NT > 0: term loop unrolled at compile time
   double2* sc = s_dyn;                                          // [ppw][nterm]
   double* s_acc = reinterpret_cast<double*>(s_dyn + ppw * nterm);  // [ppw][32]
   double* s_c0 = s_acc + ppw * 32;                               // [ppw]
@@ -284,6 +301,7 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
   const int64_t kk = active ? k : nbins - 1;
   const double* __restrict__ invE = w.invE + kk;
   const double* __restrict__ hw = w.hw + kk;
+  double W = 0.0;  // sum_n h w_n of this lane's bin, same order as k_oscprob_batch
   for (int i = 0; i < order; i += N) {
     const int nn = min(N, order - i);
     double iE[N], hv[N];
@@ -292,6 +310,9 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
       iE[n] = n < nn ? invE[(int64_t)(i + n) * nbins] : 1.0;
       hv[n] = n < nn ? hw[(int64_t)(i + n) * nbins] : 0.0;
     }
+#pragma unroll
+    for (int n = 0; n < N; ++n)
+      if (n < nn) W += hv[n];
     int q = 0;
 #if GNA_BATCH_PI_Q2
     // two points at a time: 2N independent sin^2 chains per coefficient step
@@ -301,6 +322,7 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
       double a[N], b[N];
 #pragma unroll
       for (int n = 0; n < N; ++n) a[n] = b[n] = 0.0;
+      GNA_UNROLL((NT ? NT : 1))
       for (int j = 0; j < nterm; ++j) {
         const double2 cw = cq[j], cv = cr[j];
 #pragma unroll
@@ -309,13 +331,12 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
           b[n] = fma(cv.y, gna::sin2c(cv.x, iE[n]), b[n]);
         }
       }
-      const double c0a = s_c0[q], c0b = s_c0[q + 1];
       double sa = s_acc[q * 32 + lane], sb = s_acc[(q + 1) * 32 + lane];
 #pragma unroll
       for (int n = 0; n < N; ++n)
         if (n < nn) {
-          sa = fma(hv[n], c0a - a[n], sa);
-          sb = fma(hv[n], c0b - b[n], sb);
+          sa = fma(hv[n], a[n], sa);
+          sb = fma(hv[n], b[n], sb);
         }
       s_acc[q * 32 + lane] = sa;
       s_acc[(q + 1) * 32 + lane] = sb;
@@ -326,29 +347,30 @@ __global__ void __launch_bounds__(32, GNA_BATCH_MINB) k_oscprob_batch_pi(
       double a[N];
 #pragma unroll
       for (int n = 0; n < N; ++n) a[n] = 0.0;
+      GNA_UNROLL((NT ? NT : 1))
       for (int j = 0; j < nterm; ++j) {
         const double2 cw = cq[j];
 #pragma unroll
         for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
       }
-      const double c0 = s_c0[q];
       double sv = s_acc[q * 32 + lane];
 #pragma unroll
       for (int n = 0; n < N; ++n)
-        if (n < nn) sv = fma(hv[n], c0 - a[n], sv);
+        if (n < nn) sv = fma(hv[n], a[n], sv);
       s_acc[q * 32 + lane] = sv;
     }
   }
   const double D = (data && active) ? data[k] : 1.0;
+  const double iD = 1.0 / D;  // once per lane: chi2 terms d^2 / D as d^2 * iD (no per-point divide)
   const int64_t wpp = warps_per_point_dev(nbins);
   for (int q = 0; q < np; ++q) {
     const int64_t p = p0 + q;
-    const double sv = s_acc[q * 32 + lane];
+    const double sv = fma(s_c0[q], W, -s_acc[q * 32 + lane]);  // c0 W - A
     double x2 = 0.0;
     if (active) {
       if (spectra) out_store<kOut>(spectra + p * nbins + k, sv);
       const double d = sv - D;
-      x2 = d * d / D;
+      x2 = d * d * iD;
     }
     if (w.partial) {
 #pragma unroll

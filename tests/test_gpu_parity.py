@@ -487,6 +487,63 @@ def test_batch_capturable_in_cuda_graph(gna):
     assert np.array_equal(_np(sp), ref_sp) and np.array_equal(_np(x2), ref_x2)
 
 
+def test_points_inner_batch_first_call_under_capture(gna):
+    """The points-inner launch (one baseline) sizes its grid with the occupancy API on
+    first use; in a fresh process the very first call happens inside graph capture, and
+    the replay must equal a later eager call bitwise and match the oracle."""
+    import subprocess
+    import sys
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+import paper_1804_07682_b200 as gna, synth
+g = synth.rng(72)
+P, nbins, order = 300, 1000, 10
+pts = synth.points_uniform(g, P, dict(theta12=(0.5, 0.7), theta13=(0.1, 0.2),
+                                      dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+data = synth.pseudo_data(g, edges, 1.0)
+t = lambda a: torch.tensor(np.ascontiguousarray(a, dtype=np.float64), device="cuda")
+dp = {k: t(v) for k, v in pts.items()}
+de, dd = t(edges), t(data)
+sp = torch.empty((P, nbins), dtype=torch.float64, device="cuda")
+x2 = torch.empty(P, dtype=torch.float64, device="cuda")
+ws = torch.empty(gna.oscprob_batch_workspace_size(P, 1, nbins, order) // 8 + 2,
+                 dtype=torch.float64, device="cuda")
+graph = torch.cuda.CUDAGraph()
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    with torch.cuda.graph(graph, stream=s):
+        gna.oscprob_batch(dp, [52.5], [1.0], de, order, data=dd, spectra=sp, chi2=x2,
+                          workspace=ws)
+torch.cuda.current_stream().wait_stream(s)
+graph.replay()
+torch.cuda.synchronize()
+a, b = sp.cpu().numpy().copy(), x2.cpu().numpy().copy()
+sp2, x22 = gna.oscprob_batch(dp, [52.5], [1.0], de, order, data=dd)
+assert np.array_equal(a, sp2.cpu().numpy()) and np.array_equal(b, x22.cpu().numpy())
+np.save(%r, a[[0, 151, 299]])
+np.save(%r, b[[0, 151, 299]])
+""" % (root, "/tmp/gna_cap_sp.npy", "/tmp/gna_cap_x2.npy")
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    g = synth.rng(72)
+    pts = synth.points_uniform(g, 300, dict(theta12=(0.5, 0.7), theta13=(0.1, 0.2),
+                                            dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+    edges = np.sort(g.uniform(1.0, 10.0, 1001))
+    data = synth.pseudo_data(g, edges, 1.0)
+    idx = np.array([0, 151, 299])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), [52.5], [1.0], edges, 10, data=data,
+                            nthreads=_nt())
+    sp, x2 = np.load("/tmp/gna_cap_sp.npy"), np.load("/tmp/gna_cap_x2.npy")
+    assert np.max(np.abs(sp - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2 - x2r) <= _chi2_bound(spr, data))
+
+
 def test_concurrent_calls_on_two_streams(gna):
     """Concurrent calls on disjoint outputs on two non-default streams."""
     import torch

@@ -12,10 +12,25 @@ sys.path.insert(0, ROOT)
 from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
+    "base": dict(),
+    "pi_m20": dict(GNA_BATCH_PI_MINB=20),
+    "pi_m18": dict(GNA_BATCH_PI_MINB=18),
+    "pi_m24": dict(GNA_BATCH_PI_MINB=24),
+    "pi_nt3": dict(GNA_BATCH_PI_NT=1),
+    "mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
+    "notail": dict(GNA_BATCH_PI_TAIL=0),
+    "tail_m20": dict(GNA_BATCH_PI_MINB=20),
+    "mb20_nt3": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1, GNA_BATCH_PI_NT=1),
+    "pi_nt3_m16": dict(GNA_BATCH_PI_NT=1, GNA_BATCH_PI_MINB=16),
+    "pi_m20_w240": dict(GNA_BATCH_PI_MINB=20, GNA_BATCH_PPW_WORK=240),
     "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
     "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
     "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
 }
+
+
+KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0E",
+           r"k_oscprob_batch_piILi5ELi0ELi0E", r"k_oscprob_batch_piILi5ELi0ELi3E"]
 
 
 def main(names):
@@ -27,9 +42,11 @@ def main(names):
             [_build.nvcc(), *_build.NVCC_FLAGS, *["-D%s=%s" % kv for kv in VARIANTS[name].items()],
              "-Xptxas", "-v", "-o", out, os.path.join(_build.CSRC, "gna_b200.cu")],
             capture_output=True, text=True, check=True).stderr
-        m = re.search(r"k_oscprob_eval_tmaIN3gna7PeeCoefEEvT_PKdPdl.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers",
-                      cmd_out, re.S)
-        print(name, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
+        for kern in KERNELS:
+            m = re.search(r"Compiling entry function '[^']*" + kern + r"[^']*' for 'sm_100a'\n"
+                          r"[^\n]*\n\s*\d+ bytes stack frame, (\d+) bytes spill stores[^\n]*\n"
+                          r"[^\n]*Used (\d+) registers", cmd_out)
+            print(name, kern, "regs", m.group(2) if m else "?", "spills", m.group(1) if m else "?")
 
 
 if __name__ == "__main__":
