@@ -35,13 +35,17 @@ METRIC = "energy points/sec (fp64 P_ee+GL)"
 UNIT = "energy points/s"
 
 # Algorithmic FP64-pipe work per energy point: three sin^2
-# terms x 13 FP64 instructions (rint 2, reduced argument 1, square 1, degree-8
-# minimax 8, weighted accumulate 1).  Per-node work (reciprocal, node position,
-# GL weight) is amortised over baselines and not counted.
-FP64_OPS_PER_EVAL = 39
+# terms x (degree + 5) FP64 instructions (rint 2, reduced argument 1, square 1, minimax
+# Horner `degree`, weighted accumulate 1) = 36 at the default degree 7 (39 at degree 8);
+# the degree is read from the loaded library (gna_sin2_poly_degree).  Per-node work
+# (reciprocal, node position, GL weight) is amortised over baselines and not counted.
+def fp64_ops_per_eval(deg):
+    return 3 * (deg + 5)
+
+
 # elementwise mode adds the reciprocal of each energy: MUFU.RCP64H (1/3-rate, 3 slots)
 # + 3 DFMA (tools/probe_rcp.cu)
-FP64_OPS_EVAL_MODE = FP64_OPS_PER_EVAL + 6
+RCP_OPS = 6
 FP64_LANES_PER_SM = 64        # measured: tools/probe_fp64.cu, profiles/r01_probe_fp64.jsonl
 SM_COUNT = 148
 
@@ -601,6 +605,8 @@ def main():
 
     # ---------------- roofline of the dominant kernel (batch / gl / eval)
     peak_ops = SM_COUNT * FP64_LANES_PER_SM * (clk.summary()["sm_max_mhz"] or 1965.0) * 1e6
+    deg = gna.sin2_poly_degree()
+    ops_eval = fp64_ops_per_eval(deg)
     if args.workload == "cfg4grid":
         # separable scan: the step is bound by writing the spectra (8 B per point x bin)
         out_bytes = c["bins_total"] * 8
@@ -612,8 +618,9 @@ def main():
                 "note": "whole gna_oscprob_scan call (stage-A sin^2 tables + rank-3 expansion "
                         "+ chi2 reduce); algorithmic bytes = spectra written"}
     elif args.workload == "cfg3emu":
-        # general channel: 3 pairs x 24 FP64 + reciprocal 6 + 1 = 79 FP64 slots per energy
-        ops = 3 * 24 + 6 + 1
+        # general channel: 3 pairs x (16 + degree) FP64 + reciprocal 6 + 1 slots per energy
+        # (76 at degree 7; gna_device.cuh sin2_sin_c)
+        ops = 3 * (16 + deg) + RCP_OPS + 1
         achieved = units_per_rank * ops / (kern_avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
                 "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
@@ -628,17 +635,17 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": peaks["source"],
-                "fp64_frac": launch_units * FP64_OPS_EVAL_MODE / (kern_avg_ms * 1e-3) / peak_ops,
-                "fp64_ops_per_energy": FP64_OPS_EVAL_MODE}
+                "fp64_frac": launch_units * (ops_eval + RCP_OPS) / (kern_avg_ms * 1e-3) / peak_ops,
+                "fp64_ops_per_energy": ops_eval + RCP_OPS}
     else:
         launch_units = (units_per_rank / max(calls_per_step, 1)
                         if args.workload in ("cfg4", "cfg5") else units_per_rank)
-        achieved = launch_units * FP64_OPS_PER_EVAL / (kern_avg_ms * 1e-3) / 1e12
+        achieved = launch_units * ops_eval / (kern_avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
                 "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
                 "peak_source": "148 SM x 64 FP64 lanes x sm_max clock (lanes measured by "
                                "tools/probe_fp64.cu: 18.55 T DFMA/s at 1965 MHz)",
-                "ops_per_energy_point": FP64_OPS_PER_EVAL,
+                "ops_per_energy_point": ops_eval, "sin2_poly_degree": deg,
                 "kernel_ms_per_launch": kern_avg_ms}
 
     tr = _ncu_traffic(args.workload)

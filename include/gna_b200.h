@@ -283,6 +283,11 @@ int gna_abi_version(void);
  * (diagnostics for the bench's gpu_launches count).                          */
 int64_t gna_launch_count(void);
 
+/* Degree in u = f^2 of the minimax v(u) = -cos(pi sqrt u)/2 compiled into the sin^2
+ * kernels (7: max error 1.1e-15 per term; 8: 1.1e-16).  Each sin^2 term costs
+ * degree + 5 FP64 instructions; the bench's roofline uses it.  */
+int gna_sin2_poly_degree(void);
+
 #ifdef __cplusplus
 }
 #endif

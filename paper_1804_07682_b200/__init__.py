@@ -40,6 +40,7 @@ EXPORTS = (
     "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_gl_integrate_host",
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
+    "gna_sin2_poly_degree",
     "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
     "gna_oscprob_batch_ex", "gna_gl_integrate_ab", "gna_fit_workspace_size",
     "gna_fit_pattern_search",
@@ -149,12 +150,13 @@ def load(path: str | None = None) -> ctypes.CDLL:
     L.gna_strerror.restype = ctypes.c_char_p
     L.gna_last_cuda_error.argtypes = []
     L.gna_abi_version.argtypes = []
+    L.gna_sin2_poly_degree.argtypes = []
     L.gna_launch_count.argtypes = []
     L.gna_launch_count.restype = i64
     for name in ("gna_oscprob_eval", "gna_gl_integrate", "gna_oscprob_batch",
                  "gna_oscprob_eval_host", "gna_gl_integrate_host", "gna_oscprob_batch_host",
                  "gna_gl_rule",
-                 "gna_last_cuda_error", "gna_abi_version"):
+                 "gna_last_cuda_error", "gna_abi_version", "gna_sin2_poly_degree"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -468,3 +470,8 @@ def launch_count() -> int:
 
 def abi_version() -> int:
     return int(load().gna_abi_version())
+
+
+def sin2_poly_degree() -> int:
+    """Degree of the sin^2 minimax compiled into the library (gna_sin2_poly_degree)."""
+    return int(load().gna_sin2_poly_degree())

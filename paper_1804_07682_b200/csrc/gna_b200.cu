@@ -864,5 +864,7 @@ int gna_abi_version(void) { return GNA_ABI_VERSION; }
 
 int64_t gna_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int gna_sin2_poly_degree(void) { return GNA_SIN2_DEG; }
+
 }  // extern "C"
 

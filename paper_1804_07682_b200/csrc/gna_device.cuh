@@ -5,9 +5,10 @@
 //   q  = t - 1.5*2^52           DADD  (exact)
 //   f  = kq * invE - q          DFMA  (one rounding of the exact product minus q, |f| <= 1/2)
 //   u  = f * f                  DMUL
-//   v  = V(u)                   8 DFMA (minimax, |err| <= 1.1e-16; sin2_poly.h)
+//   v  = V(u)                   7 DFMA (minimax of degree 7 in u, |err| <= 1.11e-15, V(0) = -1/2
+//                               exactly; sin2_poly.h.  GNA_SIN2_DEG 8: 8 DFMA, |err| <= 1.1e-16)
 //   acc += w * ((-1)^q v)       DFMA  (sign of v flipped with 2 integer ops on its hi word)
-// = 13 FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
+// = 12 (13) FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
 // v(f) = -cos(pi f)/2, so that sum_ij w_ij sin^2 = sum w_ij / 2 + sum w_ij (-1)^q v.
 // The reduction is exact for |y| < 2^51; the only error beyond the polynomial's is
 // the rounding of kq and invE (R7, R9).
@@ -21,14 +22,43 @@ namespace gna {
 
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 
+// Degree of the v(u) minimax (sin2_poly.h): 8 (|err| 1.1e-16) or 7 (|err| 1.1e-15, c0 = -1/2
+// pinned; one DFMA fewer per term).  DESIGN.md §6.1 and R7.
+#ifndef GNA_SIN2_DEG
+#define GNA_SIN2_DEG 7
+#endif
+
 // minimax coefficients in the constant bank: DFMA takes c[][] operands directly,
 // so the Horner chain needs no register or uniform-register moves.
+#if GNA_SIN2_DEG == 7
+__constant__ double c_sin2[8] = {GNA_SIN2_D7_C0, GNA_SIN2_D7_C1, GNA_SIN2_D7_C2, GNA_SIN2_D7_C3,
+                                 GNA_SIN2_D7_C4, GNA_SIN2_D7_C5, GNA_SIN2_D7_C6, GNA_SIN2_D7_C7};
+#elif GNA_SIN2_DEG == 8
 __constant__ double c_sin2[9] = {GNA_SIN2_C0, GNA_SIN2_C1, GNA_SIN2_C2, GNA_SIN2_C3, GNA_SIN2_C4,
                                  GNA_SIN2_C5, GNA_SIN2_C6, GNA_SIN2_C7, GNA_SIN2_C8};
+#else
+#error "GNA_SIN2_DEG must be 7 or 8"
+#endif
 // sin(pi f) = f S(f^2), S minimax of degree 8 (sinpi_poly.h; appearance channels, NEXT-2)
 __constant__ double c_sinpi[9] = {GNA_SINPI_C0, GNA_SINPI_C1, GNA_SINPI_C2, GNA_SINPI_C3,
                                   GNA_SINPI_C4, GNA_SINPI_C5, GNA_SINPI_C6, GNA_SINPI_C7,
                                   GNA_SINPI_C8};
+
+// v(u) = -cos(pi sqrt(u)) / 2 by Horner on the constant bank
+__device__ __forceinline__ double sin2_poly(double u) {
+#if GNA_SIN2_DEG == 8
+  double p = fma(u, c_sin2[8], c_sin2[7]);
+  p = fma(p, u, c_sin2[6]);
+#else
+  double p = fma(u, c_sin2[7], c_sin2[6]);
+#endif
+  p = fma(p, u, c_sin2[5]);
+  p = fma(p, u, c_sin2[4]);
+  p = fma(p, u, c_sin2[3]);
+  p = fma(p, u, c_sin2[2]);
+  p = fma(p, u, c_sin2[1]);
+  return fma(p, u, c_sin2[0]);
+}
 
 // (-1)^q * V(f^2) for y = kq * invE = q + f  (y itself is never rounded separately)
 __device__ __forceinline__ double sin2c(double kq, double invE) {
@@ -36,14 +66,7 @@ __device__ __forceinline__ double sin2c(double kq, double invE) {
   const double q = t - kRoundMagic;
   const double f = fma(kq, invE, -q);
   const double u = f * f;
-  double p = fma(u, c_sin2[8], c_sin2[7]);
-  p = fma(p, u, c_sin2[6]);
-  p = fma(p, u, c_sin2[5]);
-  p = fma(p, u, c_sin2[4]);
-  p = fma(p, u, c_sin2[3]);
-  p = fma(p, u, c_sin2[2]);
-  p = fma(p, u, c_sin2[1]);
-  p = fma(p, u, c_sin2[0]);
+  const double p = sin2_poly(u);
   // parity of q = bit 0 of t's low word -> sign bit of p
   const int odd = __double2loint(t) << 31;
   return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
@@ -63,14 +86,7 @@ __device__ __forceinline__ double sin2c_fq(double kq, float kqf, double invE, fl
   const double q = __hiloint2double(0x43380000, qi + (int)0x80000000) - kRoundMagic31;
   const double f = fma(kq, invE, -q);
   const double u = f * f;
-  double p = fma(u, c_sin2[8], c_sin2[7]);
-  p = fma(p, u, c_sin2[6]);
-  p = fma(p, u, c_sin2[5]);
-  p = fma(p, u, c_sin2[4]);
-  p = fma(p, u, c_sin2[3]);
-  p = fma(p, u, c_sin2[2]);
-  p = fma(p, u, c_sin2[1]);
-  p = fma(p, u, c_sin2[0]);
+  const double p = sin2_poly(u);
   const int odd = qi << 31;
   return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
 }
@@ -93,9 +109,13 @@ __device__ __forceinline__ double sin2_sin_c(double kq, double invE, double a, d
   const double q = t - kRoundMagic;
   const double f = fma(kq, invE, -q);
   const double u = f * f;
+#if GNA_SIN2_DEG == 8
   double p = fma(u, c_sin2[8], c_sin2[7]);
-  double r = fma(u, c_sinpi[8], c_sinpi[7]);
   p = fma(p, u, c_sin2[6]);
+#else
+  double p = fma(u, c_sin2[7], c_sin2[6]);
+#endif
+  double r = fma(u, c_sinpi[8], c_sinpi[7]);
   r = fma(r, u, c_sinpi[6]);
   p = fma(p, u, c_sin2[5]);
   r = fma(r, u, c_sinpi[5]);

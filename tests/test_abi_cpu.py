@@ -237,9 +237,9 @@ def test_gl_rule_einval(lib):
     assert lib.gna_gl_rule(33, buf.ctypes.data, buf.ctypes.data) == gna.GNA_EINVAL
 
 
-def _sin2_coeffs():
+def _sin2_coeffs(prefix="GNA_SIN2_C"):
     src = open(os.path.join(_build.CSRC, "sin2_poly.h")).read()
-    cs = dict(re.findall(r"#define GNA_SIN2_C(\d) \(([-0-9a-fx.p+]+)\)", src))
+    cs = dict(re.findall(r"#define %s(\d) \(([-0-9a-fx.p+]+)\)" % prefix, src))
     return [float.fromhex(cs[str(j)]) for j in range(len(cs))]
 
 
@@ -272,10 +272,14 @@ def _fma(a, b, c):
     return float(Fraction(a) * Fraction(b) + Fraction(c))
 
 
-def test_kernel_sin2_polynomial_accuracy():
-    """sin^2((pi/2)(q+f)) = 1/2 + (-1)^q V(f^2) with the kernel's fp64 Horner: |err| <= 1.2e-16."""
-    cf = _sin2_coeffs()
-    assert len(cf) == 9 and cf[0] == -0.5
+@pytest.mark.parametrize("prefix,ncoef,bound", [("GNA_SIN2_C", 9, 1.2e-16),
+                                                ("GNA_SIN2_D7_C", 8, 1.12e-15)])
+def test_kernel_sin2_polynomial_accuracy(prefix, ncoef, bound):
+    """sin^2((pi/2)(q+f)) = 1/2 + (-1)^q V(f^2) with the kernel's fp64 Horner: |err| <= bound
+    (degree 8: 1.2e-16; degree 7, the default: 1.12e-15 — DESIGN.md R7), plus the final
+    half-ulp of 1/2 +- v.  Both pin V(0) = -1/2, so sin^2 is exactly 0 at even q, f = 0."""
+    cf = _sin2_coeffs(prefix)
+    assert len(cf) == ncoef and cf[0] == -0.5
     mp.mp.dps = 40
     g = np.random.default_rng(3)
     fs = np.r_[np.linspace(-0.5, 0.5, 801), g.uniform(-0.5, 0.5, 400)]
@@ -289,4 +293,19 @@ def test_kernel_sin2_polynomial_accuracy():
             got = 0.5 + (p if q % 2 == 0 else -p)
             ref = mp.sin(mp.pi / 2 * (q + mp.mpf(float(f)))) ** 2
             worst = max(worst, abs(float(got - ref)))
-    assert worst <= 1.2e-16 + 1.2e-16  # polynomial + final half-ulp of 1/2 +- v
+    assert worst <= bound + 1.2e-16  # polynomial + final half-ulp of 1/2 +- v
+
+
+def test_kernel_sin2_small_phase_error_vanishes():
+    """With V(0) = -1/2 pinned, the degree-7 error is O(u): for |f| <= 1e-3 the Horner result
+    stays at the rounding level (<= 1.2e-16 (1 + 1e6 u)) instead of the 1.1e-15 worst case, so
+    small phases (short baselines, L -> 0) are exact to rounding."""
+    cf = _sin2_coeffs("GNA_SIN2_D7_C")
+    mp.mp.dps = 40
+    for f in np.linspace(-1e-3, 1e-3, 101):
+        u = float(f) * float(f)
+        p = cf[-1]
+        for c in reversed(cf[:-1]):
+            p = _fma(p, u, c)
+        ref = -mp.cos(mp.pi * mp.mpf(float(f))) / 2
+        assert abs(float(p - ref)) <= 1.2e-16 * (1 + 1e6 * u)

@@ -75,6 +75,43 @@ def remez(deg, iters=8):
     return c
 
 
+def remez_c0(deg, iters=12):
+    """Minimax of V on [0, 1/4] with the constant term pinned to V(0) = -1/2 exactly, so that
+    sin^2 is exactly 0 at every even multiple of pi/2 (f = 0) and the error vanishes like u
+    near there.  Unknowns c1..cdeg and the levelled error E; alternation points in (0, 1/4]."""
+    n = deg + 1
+    xs = [B * (1 - mp.cos(mp.pi * (k + 1) / n)) / 2 for k in range(n)]
+    c = None
+    for _ in range(iters):
+        M = mp.matrix([[x ** j for j in range(1, deg + 1)] + [(-1) ** k] for k, x in enumerate(xs)])
+        y = mp.matrix([V(x) + mp.mpf(1) / 2 for x in xs])
+        sol = mp.lu_solve(M, y)
+        c = [mp.mpf(-1) / 2] + [sol[j] for j in range(deg)]
+        grid = [A + (B - A) * mp.mpf(i) / 4000 for i in range(1, 4001)]
+        err = [sum(c[j] * g ** j for j in range(deg + 1)) - V(g) for g in grid]
+        ext = []
+        i = 0
+        while i < len(grid):
+            s = mp.sign(err[i]) or 1
+            j = i
+            best = i
+            while j < len(grid) and (mp.sign(err[j]) or 1) == s:
+                if abs(err[j]) > abs(err[best]):
+                    best = j
+                j += 1
+            ext.append(best)
+            i = j
+        if len(ext) < n:
+            break
+        while len(ext) > n:
+            if abs(err[ext[0]]) < abs(err[ext[-1]]):
+                ext.pop(0)
+            else:
+                ext.pop()
+        xs = [grid[k] for k in ext]
+    return c
+
+
 def fma(a: float, b: float, c: float) -> float:
     return float(Fraction(a) * Fraction(b) + Fraction(c))
 
@@ -148,18 +185,24 @@ def main():
         cf = [float(x) for x in c]
         results[deg] = (cf, max_err(cf))
         print("degree", deg, "max |err| fp64 Horner:", results[deg][1], file=sys.stderr)
-    deg = 8
-    cf, err = results[deg]
+    cf, err = results[8]
+    cf7 = [float(x) for x in remez_c0(7)]
+    err7 = max_err(cf7)
+    print("degree 7 (c0 = -1/2 pinned) max |err| fp64 Horner:", err7, file=sys.stderr)
     lines = [
         "// GENERATED by tools/gen_sin2_poly.py — do not edit.",
-        "// v(u) = -cos(pi*sqrt(u))/2 on u in [0, 1/4] (u = f^2, |f| <= 1/2), minimax degree %d." % deg,
+        "// v(u) = -cos(pi*sqrt(u))/2 on u in [0, 1/4] (u = f^2, |f| <= 1/2), minimax.",
         "// sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f^2).  Max abs error of the fp64 FMA Horner",
-        "// evaluation vs 60-digit mpmath on 4001 points: %.3e." % err,
+        "// evaluation vs 60-digit mpmath on 4001 points: degree 8 %.3e, degree 7 %.3e." % (err, err7),
+        "// Degree 7 (GNA_SIN2_D7_*) has c0 = -1/2 pinned: sin^2 = 0 exactly at f = 0.",
         "#pragma once",
-        "#define GNA_SIN2_POLY_DEG %d" % deg,
+        "#define GNA_SIN2_ERR8 %.3e" % err,
+        "#define GNA_SIN2_ERR7 %.3e" % err7,
     ]
     for j, x in enumerate(cf):
         lines.append("#define GNA_SIN2_C%d (%s)  /* %.17g */" % (j, x.hex(), x))
+    for j, x in enumerate(cf7):
+        lines.append("#define GNA_SIN2_D7_C%d (%s)  /* %.17g */" % (j, x.hex(), x))
     open(out, "w").write("\n".join(lines) + "\n")
     print("wrote", out, "err", err, file=sys.stderr)
 

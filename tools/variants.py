@@ -17,6 +17,7 @@ VARIANTS = {
     "pi_m18": dict(GNA_BATCH_PI_MINB=18),
     "pi_m24": dict(GNA_BATCH_PI_MINB=24),
     "pi_nt3": dict(GNA_BATCH_PI_NT=1),
+    "deg7": dict(GNA_SIN2_DEG=7),
     "mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
     "notail": dict(GNA_BATCH_PI_TAIL=0),
     "tail_m20": dict(GNA_BATCH_PI_MINB=20),
