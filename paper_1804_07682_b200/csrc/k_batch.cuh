@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #define GNA_BATCH_LDS_PREFETCH 0
 #endif
 #ifndef GNA_BATCH_JUNROLL
-#define GNA_BATCH_JUNROLL 1
+#define GNA_BATCH_JUNROLL 2
 #endif
 #ifndef GNA_BATCH_MINB
 #define GNA_BATCH_MINB 1

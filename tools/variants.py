@@ -13,6 +13,15 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "base": dict(),
+    "d7_mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
+    "d7_mb18": dict(GNA_BATCH_MINB=18, GNA_BATCH_PI_MINB=1),
+    "d7_ju2": dict(GNA_BATCH_JUNROLL=2),
+    "d7_ju3": dict(GNA_BATCH_JUNROLL=3),
+    "d7_ju4": dict(GNA_BATCH_JUNROLL=4),
+    "d7_ju8": dict(GNA_BATCH_JUNROLL=8),
+    "d7_ju2_mb20": dict(GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
+    "d7_pim20": dict(GNA_BATCH_PI_MINB=20),
+    "d7_lds": dict(GNA_BATCH_LDS_PREFETCH=1),
     "pi_m20": dict(GNA_BATCH_PI_MINB=20),
     "pi_m18": dict(GNA_BATCH_PI_MINB=18),
     "pi_m24": dict(GNA_BATCH_PI_MINB=24),
