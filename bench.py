@@ -43,6 +43,9 @@ def fp64_ops_per_eval(deg):
     return 3 * (deg + 5)
 
 
+# mixed tier (NEXT-3): instructions per sin^2 term (3 FP64 + F2F + 4 per chain of a packed
+# FFMA2 pair), DESIGN.md §6.8
+MIXED_INSTR_PER_TERM = 8
 # elementwise mode adds the reciprocal of each energy: MUFU.RCP64H (1/3-rate, 3 slots)
 # + 3 DFMA (tools/probe_rcp.cu)
 RCP_OPS = 6
@@ -64,6 +67,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--lib", default=None, help="alternative libgna_b200.so (tuning variants)")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"],
+                    help="cfg4/cfg5 batch tier: fp64 (default, 1e-11) or the NEXT-3 mixed tier "
+                         "(GNA_PREC_MIXED: fp64 phases, fp32 polynomial; 1e-5)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend (gloo only to exercise the N>1 code path on "
                          "one GPU, with GNA_BENCH_SAME_DEVICE=1; not for measurements)")
@@ -71,7 +77,10 @@ def parse():
                     help="N>1 exchange: fused kernel-epilogue stores (validated) or NCCL all-gather")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as a CUDA graph (auto: when N == 1)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.precision == "mixed" and (a.workload not in ("cfg4", "cfg5") or a.impl != "ours"):
+        ap.error("--precision mixed applies to the cfg4/cfg5 batch of --impl ours")
+    return a
 
 
 # ----------------------------------------------------------------------------- workloads
@@ -390,7 +399,7 @@ def main():
             sub = {k: v[vlo:vhi] for k, v in pts.items()}
             with KernelTimer(kern_ev):
                 gna.oscprob_batch(sub, L, om, edges, c["order"], data=data, spectra=sp_rows,
-                                  chi2=x2_rows, workspace=ws)
+                                  chi2=x2_rows, workspace=ws, precision=args.precision)
 
         def step():
             sb.step(compute, comm_stream=comm)
@@ -410,6 +419,8 @@ def main():
             dist.all_reduce(built, op=dist.ReduceOp.MIN)
             if float(built) == 1.0:
                 sp_ptr, x2_ptr, fflags = fg.out_ptrs()
+                if args.precision == "mixed":
+                    fflags |= gna.GNA_PREC_MIXED
 
                 def step_fused():
                     with KernelTimer(kern_ev):
@@ -647,8 +658,23 @@ def main():
                                "tools/probe_fp64.cu: 18.55 T DFMA/s at 1965 MHz)",
                 "ops_per_energy_point": ops_eval, "sin2_poly_degree": deg,
                 "kernel_ms_per_launch": kern_avg_ms}
+        if args.precision == "mixed":
+            # NEXT-3 mixed tier: the work spreads over the FP64, XU and FMA
+            # pipes, so the roofline is instruction issue (1 warp instruction per SMSP per cycle
+            # = 148 x 4 x 32 lanes x clock).  Per sin^2 term: 3 FP64 (rint of y/2, m, h) + 1 F2F
+            # + half of a packed pair's FMUL2 + 6 FFMA2 + accumulating FFMA2 = 8.
+            ipp = 3 * MIXED_INSTR_PER_TERM
+            peak_issue = SM_COUNT * 4 * 32 * (clk.summary()["sm_max_mhz"] or 1965.0) * 1e6
+            ach = launch_units * ipp / (kern_avg_ms * 1e-3)
+            roof = {"bound": "alu", "achieved": ach / 1e12, "peak": peak_issue / 1e12,
+                    "unit": "T instr/s (issue)", "frac": ach / peak_issue, "traffic": None,
+                    "peak_source": "148 SM x 4 SMSP x 32 lanes x sm_max clock (one warp "
+                                   "instruction per SMSP per cycle)",
+                    "ops_per_energy_point": ipp,
+                    "fp64_frac": launch_units * 9 / (kern_avg_ms * 1e-3) / peak_ops,
+                    "kernel_ms_per_launch": kern_avg_ms}
 
-    tr = _ncu_traffic(args.workload)
+    tr = _ncu_traffic(args.workload if args.precision == "fp64" else args.workload + "_mixed")
     if tr:
         roof["traffic"] = tr["bytes"]
         roof["traffic_source"] = tr["source"]
@@ -656,7 +682,9 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if scaling == "strong" else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f64 phases + f32 polynomial (mixed tier)",
+            "data": "synthetic",
             "config": dict(c["desc"], parallelism="dp%d over parameter points" % world
                            if scaling == "strong" else "replicas x%d" % world,
                            l2="flushed between steps (256 MiB write, untimed)",
@@ -673,8 +701,14 @@ def main():
                 args, c, gna, torch, dist, dev, rank, sb, fused_fg if gather_mode.startswith(
                     "fused") else None)
 
+    if args.precision == "mixed":
+        line["config"]["precision"] = "mixed (GNA_PREC_MIXED, tier tolerance 1e-5 relative)"
+        line["mixed_vs_fp64"] = _mixed_accuracy(c, gna, torch, dev) if rank == 0 else None
     # ---------------- e2e: host buffers through the C ABI, copies inside the timed region
-    if not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu", "cfg5fit"):
+    if args.precision == "mixed":
+        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0, "note": "host-buffer API is fp64-only"}
+    elif not args.no_e2e and args.workload not in ("cfg4grid", "cfg3emu", "cfg5fit"):
         line["e2e"] = e2e(args, c, gna, torch, dist, dev, world, rank, local)
     elif args.workload in ("cfg4grid", "cfg3emu", "cfg5fit"):
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -700,6 +734,20 @@ def main():
         dist.destroy_process_group()
 
 
+def _mixed_accuracy(c, gna, torch, dev):
+    """Max relative deviation of the mixed-tier spectra from the fp64 path on this workload
+    (both on the GPU, outside the timed region; the fp64 path is itself within 1e-11 of the
+    oracle)."""
+    f64 = dict(dtype=torch.float64, device=dev)
+    pts = {k: torch.tensor(v, **f64) for k, v in c["points"].items()}
+    args = (pts, c["L_km"], c["omega"], torch.tensor(c["edges"], **f64), c["order"])
+    d = torch.tensor(c["data"], **f64)
+    s64, x64 = gna.oscprob_batch(*args, data=d)
+    smx, xmx = gna.oscprob_batch(*args, data=d, precision="mixed")
+    return {"spectra_max_rel": float(((smx - s64).abs() / s64.abs()).max()),
+            "chi2_max_rel": float(((xmx - x64).abs() / x64.abs()).max())}
+
+
 def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
     """Rank 0: gathered spectra/chi2 == one batch over all points on this GPU (bitwise)."""
     ok = torch.ones(1, device=dev)
@@ -707,7 +755,8 @@ def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
         f64 = dict(dtype=torch.float64, device=dev)
         pts = {k: torch.tensor(v, **f64) for k, v in c["points"].items()}
         sp, x2 = gna.oscprob_batch(pts, c["L_km"], c["omega"], torch.tensor(c["edges"], **f64),
-                                   c["order"], data=torch.tensor(c["data"], **f64))
+                                   c["order"], data=torch.tensor(c["data"], **f64),
+                                   precision=args.precision)
         gs, gx = (fg.spectra, fg.chi2) if fg is not None else sb.gathered()
         ok.fill_(1.0 if (torch.equal(gs, sp) and torch.equal(gx, x2)) else 0.0)
         del pts, sp, x2

@@ -173,7 +173,10 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
  *   flags = GNA_OUT_PEER       outputs are peer-mapped unicast addresses (e.g. the
  *                              root's buffer): plain stores + a system-scope fence;
  *   flags = GNA_OUT_MULTICAST  outputs are NVLS multicast addresses: multimem.st
- *                              writes every participating GPU's copy (all-gather).
+ *                              writes every participating GPU's copy (all-gather);
+ *   | GNA_PREC_MIXED           the mixed-precision tier below (with flags = GNA_PREC_MIXED
+ *                              alone the outputs are local device memory, validated as
+ *                              in gna_oscprob_batch).
  * The caller synchronises the ranks after the call (e.g. a symmetric-memory or
  * NCCL barrier on the stream) before reading the gathered result.  Inputs and the
  * workspace must be this GPU's memory; output pointers are not type-checked.
@@ -182,6 +185,16 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
  * ------------------------------------------------------------------------- */
 #define GNA_OUT_PEER 1u
 #define GNA_OUT_MULTICAST 2u
+/* Mixed-precision tier (the paper's single-precision remark,
+ * P:691-694), combinable with either output flag: the phases y = kq/E and their
+ * reduction modulo 2 (y = 2m + 2h, |h| <= 1/2) stay fp64; h is rounded to fp32,
+ * -cos(pi y)/2 = -cos(2 pi h)/2 is an fp32 degree-6 minimax evaluated two chains
+ * at a time (packed FFMA2), and the terms of one node are summed in fp32 (weights
+ * rounded to fp32); node, bin and chi^2 sums stay fp64.  Error per sin^2 term
+ * <= 2.3e-7; spectra are tested against the oracle at 1e-5 relative (tier
+ * tolerance; measured <= 8.2e-7 on cfg4/cfg5) — not the
+ * 1e-12 / 1e-11 of the default path.                                            */
+#define GNA_PREC_MIXED 4u
 
 int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const double* omega,
                          int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,

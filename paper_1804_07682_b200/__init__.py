@@ -27,7 +27,7 @@ __all__ = [
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
     "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab", "oscprob_batch_ex",
     "gl_integrate_ab", "fit_pattern_search", "fit_workspace_size",
-    "GNA_OUT_PEER", "GNA_OUT_MULTICAST",
+    "GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED",
 ]
 
 GNA_OK, GNA_EINVAL, GNA_ECUDA, GNA_ENODEV, GNA_ENOMEM = 0, -1, -2, -3, -4
@@ -48,6 +48,7 @@ EXPORTS = (
 
 GNA_OUT_PEER = 1
 GNA_OUT_MULTICAST = 2
+GNA_PREC_MIXED = 4
 
 
 class GnaError(RuntimeError):
@@ -265,14 +266,18 @@ def oscprob_batch_workspace_size(npoints: int, nbase: int, nbins: int, order: in
 
 
 def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spectra=True,
-                  chi2=None, workspace=None, stream=None):
+                  chi2=None, workspace=None, stream=None, precision: str = "fp64"):
     """Batched spectra and chi^2 (gna_oscprob_batch).
 
     points: dict of CUDA float64 tensors theta12, theta13, dm2_21, dm2_31 [P].
     spectra: True to allocate, a [P, nbins] tensor to fill, or None/False.
     chi2: computed when `data` is given (a [P] tensor may be passed to fill).
+    precision: "fp64" (gna_oscprob_batch, the 1e-11 tier) or "mixed" (gna_oscprob_batch_ex
+    with GNA_PREC_MIXED: fp64 phases, fp32 polynomial and term sums; 1e-6 tier).
     Returns (spectra or None, chi2 or None).
     """
+    if precision not in ("fp64", "mixed"):
+        raise ValueError("precision must be 'fp64' or 'mixed'")
     import torch
     L = load()
     P = points["theta12"].numel()
@@ -291,13 +296,16 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
     b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
     if Lh.size != om.size:
         raise ValueError("L_km and omega must have the same length")
-    _check(L.gna_oscprob_batch(
-        ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins,
-        int(order), _dev(spectra, "spectra", P * nbins) if spectra is not None else None,
-        _dev(data, "data", nbins) if data is not None else None,
-        _dev(chi2, "chi2", P) if chi2 is not None else None,
-        _dev(workspace, "workspace"), workspace.numel() * 8, _stream(stream)),
-        "gna_oscprob_batch")
+    args = (ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"),
+            nbins, int(order), _dev(spectra, "spectra", P * nbins) if spectra is not None else None,
+            _dev(data, "data", nbins) if data is not None else None,
+            _dev(chi2, "chi2", P) if chi2 is not None else None,
+            _dev(workspace, "workspace"), workspace.numel() * 8)
+    if precision == "mixed":
+        _check(L.gna_oscprob_batch_ex(*args, GNA_PREC_MIXED, _stream(stream)),
+               "gna_oscprob_batch_ex")
+    else:
+        _check(L.gna_oscprob_batch(*args, _stream(stream)), "gna_oscprob_batch")
     return spectra, chi2
 
 

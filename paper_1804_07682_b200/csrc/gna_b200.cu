@@ -218,7 +218,7 @@ int64_t blocks_per_point(int64_t nbins) {
 }
 
 // launch of the batch kernels on already-validated device arguments
-template <int kOut>
+template <int kOut, bool kMixed>
 int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double* omega,
                    int32_t nbase, const double* edges, int64_t nbins, int32_t order,
                    double* spectra, const double* data, double* chi2, void* workspace,
@@ -262,24 +262,24 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   const size_t smem = (size_t)kBatchWarps * (GNA_SIN2_FQ ? nterm + (nterm + 3) / 4 : nterm) *
                       sizeof(double2);
   // node-group size: 5, 4 or 3 when it divides the order, else 4
-  auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5, kOut>
-              : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut>
-              : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut>
-                                 : k_oscprob_batch<kBatchWarps, 4, kOut>;
+  auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5, kOut, kMixed>
+              : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut, kMixed>
+              : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut, kMixed>
+                                 : k_oscprob_batch<kBatchWarps, 4, kOut, kMixed>;
   if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
     // several points per warp: node groups outer, points inner (bitwise-identical sums)
     ppw = std::min<int64_t>(ppw, kMaxPPW);
-    auto kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut>
-               : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut>
-               : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut>
-                                  : k_oscprob_batch_pi<4, kOut>;
+    auto kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut, 0, kMixed>
+               : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut, 0, kMixed>
+               : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut, 0, kMixed>
+                                  : k_oscprob_batch_pi<4, kOut, 0, kMixed>;
 #if GNA_BATCH_PI_NT
     // single baseline (3 terms): term loop unrolled at compile time
     if (nterm == 3)
-      kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut, 3>
-            : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut, 3>
-            : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut, 3>
-                               : k_oscprob_batch_pi<4, kOut, 3>;
+      kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut, 3, kMixed>
+            : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut, 3, kMixed>
+            : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut, 3, kMixed>
+                               : k_oscprob_batch_pi<4, kOut, 3, kMixed>;
 #endif
 #if GNA_BATCH_PI_TAIL
     // Few waves (e.g. cfg4: ~8): pick the points per warp in [ppw/2, ppw] that minimises
@@ -326,15 +326,18 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
 int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
                  int32_t nbase, const double* edges, int64_t nbins, int32_t order,
                  double* spectra, const double* data, double* chi2, void* workspace,
-                 cudaStream_t s, int out_mode = kOutLocal) {
-  if (out_mode == kOutMulticast)
-    return launch_batch_k<kOutMulticast>(pts, L_km, omega, nbase, edges, nbins, order, spectra,
-                                         data, chi2, workspace, s);
-  if (out_mode == kOutPeer)
-    return launch_batch_k<kOutPeer>(pts, L_km, omega, nbase, edges, nbins, order, spectra, data,
-                                    chi2, workspace, s);
-  return launch_batch_k<kOutLocal>(pts, L_km, omega, nbase, edges, nbins, order, spectra, data,
-                                   chi2, workspace, s);
+                 cudaStream_t s, int out_mode = kOutLocal, bool mixed = false) {
+#define GNA_LB(M, X) launch_batch_k<M, X>(pts, L_km, omega, nbase, edges, nbins, order, spectra, \
+                                          data, chi2, workspace, s)
+  if (mixed) {
+    if (out_mode == kOutMulticast) return GNA_LB(kOutMulticast, true);
+    if (out_mode == kOutPeer) return GNA_LB(kOutPeer, true);
+    return GNA_LB(kOutLocal, true);
+  }
+  if (out_mode == kOutMulticast) return GNA_LB(kOutMulticast, false);
+  if (out_mode == kOutPeer) return GNA_LB(kOutPeer, false);
+  return GNA_LB(kOutLocal, false);
+#undef GNA_LB
 }
 
 int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega, int32_t nbase,
@@ -554,10 +557,11 @@ size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t 
   return batch_ws_bytes(npoints, nbase, nbins, order, true);
 }
 
-int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
-                      int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
-                      double* d_spectra, const double* d_data, double* d_chi2,
-                      void* d_workspace, size_t workspace_bytes, void* stream) {
+// gna_oscprob_batch and the local-output case of gna_oscprob_batch_ex (fp64 or mixed tier)
+static int batch_local(const gna_param_batch* pts, const double* L_km, const double* omega,
+                       int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                       double* d_spectra, const double* d_data, double* d_chi2,
+                       void* d_workspace, size_t workspace_bytes, void* stream, bool mixed) {
   int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
                           d_chi2);
   if (rc) return rc;
@@ -581,7 +585,15 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
   for (const void* q : ptrs)
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
-                      d_workspace, (cudaStream_t)stream);
+                      d_workspace, (cudaStream_t)stream, kOutLocal, mixed);
+}
+
+int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
+                      int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
+                      double* d_spectra, const double* d_data, double* d_chi2,
+                      void* d_workspace, size_t workspace_bytes, void* stream) {
+  return batch_local(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
+                     d_workspace, workspace_bytes, stream, false);
 }
 
 size_t gna_oscprob_scan_workspace_size(int64_t nmix, int64_t nmass, int64_t nbins) {
@@ -670,12 +682,13 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
                          double* d_spectra, const double* d_data, double* d_chi2,
                          void* d_workspace, size_t workspace_bytes, uint32_t flags,
                          void* stream) {
-  const uint32_t known = GNA_OUT_PEER | GNA_OUT_MULTICAST;
+  const uint32_t known = GNA_OUT_PEER | GNA_OUT_MULTICAST | GNA_PREC_MIXED;
   if ((flags & ~known) || ((flags & GNA_OUT_PEER) && (flags & GNA_OUT_MULTICAST)))
     return GNA_EINVAL;
-  if (flags == 0)
-    return gna_oscprob_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
-                             d_chi2, d_workspace, workspace_bytes, stream);
+  const bool mixed = (flags & GNA_PREC_MIXED) != 0;
+  if ((flags & (GNA_OUT_PEER | GNA_OUT_MULTICAST)) == 0)
+    return batch_local(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
+                       d_workspace, workspace_bytes, stream, mixed);
   int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
                           d_chi2);
   if (rc) return rc;
@@ -691,7 +704,7 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
                       d_workspace, (cudaStream_t)stream,
-                      (flags & GNA_OUT_MULTICAST) ? kOutMulticast : kOutPeer);
+                      (flags & GNA_OUT_MULTICAST) ? kOutMulticast : kOutPeer, mixed);
 }
 
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,

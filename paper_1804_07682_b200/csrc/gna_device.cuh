@@ -91,6 +91,100 @@ __device__ __forceinline__ double sin2c_fq(double kq, float kqf, double invE, fl
   return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
 }
 
+// Mixed tier.  The phase y = kq/E and its reduction stay
+// fp64 — they need it: y reaches ~1e3 and fp32 would lose the phase (ulp(550) = 6e-5).  The
+// reduction is taken modulo 2, y = 2m + 2h with m = rint(y/2), |h| <= 1/2 (three FP64
+// instructions on kqh = kq/2, staged exactly), so that (-1)^q v(f) = -cos(pi y)/2 =
+// -cos(2 pi h)/2 = W(h^2) needs no sign flip; h is rounded to fp32 (F2F) and W is a degree-6
+// fp32 minimax (|err| 1.3e-7, sin2_poly.h).  Two chains are evaluated per instruction with
+// sm_100a's packed FP32 FMA (FFMA2): per pair of terms 2 x (3 FP64 + F2F) + FMUL2 + 6 FFMA2
+// + the accumulating FFMA2 = 16 instructions, 8 per term (the fp64 path: 12).
+__constant__ float c_cos2f[7] = {GNA_COS2F_C0, GNA_COS2F_C1, GNA_COS2F_C2, GNA_COS2F_C3,
+                                 GNA_COS2F_C4, GNA_COS2F_C5, GNA_COS2F_C6};
+
+typedef unsigned long long f32x2;  // two fp32 lanes in one 64-bit register pair
+
+__device__ __forceinline__ f32x2 f2_pack(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(f32x2 v) { return __int_as_float((int)(unsigned)v); }
+__device__ __forceinline__ float f2_hi(f32x2 v) { return __int_as_float((int)(unsigned)(v >> 32)); }
+__device__ __forceinline__ f32x2 f2_fma(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+#ifndef GNA_MIXED_CVT
+#define GNA_MIXED_CVT 0
+#endif
+
+// h = y/2 - rint(y/2) for y/2 = kqh * invE, rounded to fp32 by F2F (XU pipe, ~16 lanes/SM)
+__device__ __forceinline__ float mixed_h(double kqh, double invE) {
+  const double t = fma(kqh, invE, kRoundMagic);
+  const double m = t - kRoundMagic;
+  return __double2float_rn(fma(kqh, invE, -m));
+}
+
+// The same h without a conversion instruction: the last FMA adds 1.5 * 2^29 - m instead of -m,
+// so the result C + h is rounded to the 2^-23 grid and its low word holds k = round(h 2^23)
+// (two's complement, |k| <= 2^22); C2 - t = 1.5*2^29 - m is exact.  The caller turns k into
+// fp32 with an integer add into 1.5*2^23's bit pattern and one (packed) FMA:
+// X = 1.5*2^23 + k exactly, h = X * 2^-23 - 1.5.  |h - h_fp64| <= 2^-24.
+constexpr double kRoundMagic29 = 6755400246362112.0;  // 1.5*2^52 + 1.5*2^29
+__device__ __forceinline__ int mixed_k(double kqh, double invE) {
+  const double t = fma(kqh, invE, kRoundMagic);
+  return __double2loint(fma(kqh, invE, kRoundMagic29 - t));
+}
+__device__ __forceinline__ float k_bits(int k) { return __int_as_float(0x4B400000 + k); }
+
+// fp32 h of one chain / of two chains packed, by the configured conversion
+__device__ __forceinline__ float mixed_h1(double kqh, double invE) {
+#if GNA_MIXED_CVT
+  return fmaf(k_bits(mixed_k(kqh, invE)), 0x1p-23f, -1.5f);
+#else
+  return mixed_h(kqh, invE);
+#endif
+}
+
+// W(h^2) = -cos(2 pi h)/2 for one chain
+__device__ __forceinline__ float cos2_w(float h) {
+  const float u = h * h;
+  float p = fmaf(u, c_cos2f[6], c_cos2f[5]);
+  p = fmaf(p, u, c_cos2f[4]);
+  p = fmaf(p, u, c_cos2f[3]);
+  p = fmaf(p, u, c_cos2f[2]);
+  p = fmaf(p, u, c_cos2f[1]);
+  return fmaf(p, u, c_cos2f[0]);
+}
+
+__device__ __forceinline__ f32x2 mixed_h2(double kqa, double iEa, double kqb, double iEb) {
+#if GNA_MIXED_CVT
+  return f2_fma(f2_pack(k_bits(mixed_k(kqa, iEa)), k_bits(mixed_k(kqb, iEb))),
+                f2_pack(0x1p-23f, 0x1p-23f), f2_pack(-1.5f, -1.5f));
+#else
+  return f2_pack(mixed_h(kqa, iEa), mixed_h(kqb, iEb));
+#endif
+}
+
+// the same for two chains packed in one register pair
+__device__ __forceinline__ f32x2 cos2_w2(f32x2 h2) {
+  const f32x2 u = f2_mul(h2, h2);
+  f32x2 p = f2_fma(u, f2_pack(c_cos2f[6], c_cos2f[6]), f2_pack(c_cos2f[5], c_cos2f[5]));
+  p = f2_fma(p, u, f2_pack(c_cos2f[4], c_cos2f[4]));
+  p = f2_fma(p, u, f2_pack(c_cos2f[3], c_cos2f[3]));
+  p = f2_fma(p, u, f2_pack(c_cos2f[2], c_cos2f[2]));
+  p = f2_fma(p, u, f2_pack(c_cos2f[1], c_cos2f[1]));
+  return f2_fma(p, u, f2_pack(c_cos2f[0], c_cos2f[0]));
+}
+
 // 1/x for x > 0 (normal): MUFU.RCP64H seed (measured 20 bits, tools/probe_rcp.cu,
 // profiles/r01_probe_rcp.jsonl) + one cubically convergent step r(1 + e + e^2),
 // e = 1 - x r: 3 DFMA, max error 1 ulp (2.2e-16 relative) over 1-10 MeV.

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 
 // N GL nodes of one bin at a time: each (kq, omega*w) coefficient load from
 // shared memory feeds N independent sin^2 chains (ILP across nodes).
-template <int N>
+template <int N, bool kMixed = false>
 __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int nterm,
                                             const double* __restrict__ invE,
                                             const double* __restrict__ hw, int64_t nbins, int i,
@@ -142,6 +142,35 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     iE[n] = invE[(int64_t)(i + n) * nbins];
     a[n] = 0.0;
   }
+  if constexpr (kMixed) {
+    // NEXT-3 mixed tier: y/2 reduced in fp64, W(h^2) and the per-node term sum in fp32, two
+    // nodes per packed FFMA2 (an odd last node runs scalar); one conversion to fp64 per node.
+    // Rows are staged as (kq/2, omega w as fp32 in both halves of .y).
+    constexpr int NP = N / 2;
+    gna::f32x2 acc2[NP > 0 ? NP : 1];
+    float acc1 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) acc2[k] = 0ull;
+    GNA_UNROLL(GNA_BATCH_JUNROLL)
+    for (int j = 0; j < nterm; ++j) {
+      const double2 cw = sc[j];
+      const gna::f32x2 w2 = (gna::f32x2)__double_as_longlong(cw.y);
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const gna::f32x2 h2 = gna::mixed_h2(cw.x, iE[2 * k], cw.x, iE[2 * k + 1]);
+        acc2[k] = gna::f2_fma(w2, gna::cos2_w2(h2), acc2[k]);
+      }
+      if constexpr (N & 1)
+        acc1 = fmaf(__int_as_float(__double2loint(cw.y)), gna::cos2_w(gna::mixed_h1(cw.x, iE[N - 1])),
+                    acc1);
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      a[2 * k] = (double)gna::f2_lo(acc2[k]);
+      a[2 * k + 1] = (double)gna::f2_hi(acc2[k]);
+    }
+    if constexpr (N & 1) a[N - 1] = (double)acc1;
+  } else {
 #if GNA_SIN2_FQ
   // q on the FP32 pipe: fp32 copies of the coefficients sit right after the double2 row
   const float* __restrict__ scf = reinterpret_cast<const float*>(sc + nterm);
@@ -173,6 +202,7 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
   }
 #endif
+  }
 #pragma unroll
   for (int n = 0; n < N; ++n) {
     const double h = hw[(int64_t)(i + n) * nbins];
@@ -182,18 +212,29 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
 }
 
 // remainder of r < N nodes, compile-time group size
-template <int N>
+template <int N, bool kMixed = false>
 __device__ __forceinline__ void batch_tail(int r, const double2* __restrict__ sc, int nterm,
                                            const double* __restrict__ invE,
                                            const double* __restrict__ hw, int64_t nbins, int i,
                                            double& W, double& A) {
   if constexpr (N > 1) {
     if (r == N - 1) {
-      batch_nodes<N - 1>(sc, nterm, invE, hw, nbins, i, W, A);
+      batch_nodes<N - 1, kMixed>(sc, nterm, invE, hw, nbins, i, W, A);
       return;
     }
-    batch_tail<N - 1>(r, sc, nterm, invE, hw, nbins, i, W, A);
+    batch_tail<N - 1, kMixed>(r, sc, nterm, invE, hw, nbins, i, W, A);
   }
+}
+
+// coefficient row entry as staged in shared memory: fp64 (kq, omega w), or for the mixed
+// tier kq/2 in fp64 and omega w as fp32 in both 32-bit halves of .y (a packed pair)
+template <bool kMixed>
+__device__ __forceinline__ double2 stage_coef(double2 c) {
+  if constexpr (kMixed) {
+    const int wb = __float_as_int(__double2float_rn(c.y));
+    c = make_double2(0.5 * c.x, __hiloint2double(wb, wb));  // kq/2 is exact
+  }
+  return c;
 }
 
 // Output stores of the batch epilogue (NEXT-4, fused gather):
@@ -216,7 +257,7 @@ __device__ __forceinline__ void out_store(double* p, double v) {
 // independent (no block barrier): it copies its point's coefficient row into a
 // warp-private smem slice, then each lane integrates one bin, N GL nodes at a time
 // (N divides the order when possible, so no group runs with reduced ILP).
-template <int kWarps, int N, int kOut>
+template <int kWarps, int N, int kOut, bool kMixed = false>
 __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     int nterm, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
@@ -241,7 +282,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     const double2* __restrict__ gc = w.coef + p * nterm;
     __syncwarp();  // previous point's reads of sc are done
     for (int j = lane; j < nterm; j += 32) {
-      sc[j] = gc[j];
+      sc[j] = stage_coef<kMixed>(gc[j]);
 #if GNA_SIN2_FQ
       reinterpret_cast<float*>(sc + nterm)[j] = __double2float_rn(gc[j].x);
 #endif
@@ -251,8 +292,8 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     // (one FP64 op per node instead of two)
     double W = 0.0, A = 0.0;
     int i = 0;
-    for (; i + N <= order; i += N) batch_nodes<N>(sc, nterm, invE, hw, nbins, i, W, A);
-    if (i < order) batch_tail<N>(order - i, sc, nterm, invE, hw, nbins, i, W, A);
+    for (; i + N <= order; i += N) batch_nodes<N, kMixed>(sc, nterm, invE, hw, nbins, i, W, A);
+    if (i < order) batch_tail<N, kMixed>(order - i, sc, nterm, invE, hw, nbins, i, W, A);
     const double s = fma(w.c0[p], W, -A);
     double x2 = 0.0;
     if (active) {
@@ -276,7 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
 // as k_oscprob_batch, so the results are bitwise identical.
 constexpr int kMaxPPW = 16;
 
-template <int N, int kOut, int NT = 0>
+template <int N, int kOut, int NT = 0, bool kMixed = false>
 __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
     int nterm_rt, int order, int64_t nbins, int64_t npoints, int64_t bpp, int ppw, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
@@ -292,7 +333,7 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
   if (k0 >= nbins) return;
   const int64_t p0 = pg * (int64_t)ppw;
   const int np = (int)min((int64_t)ppw, npoints - p0);
-  for (int j = lane; j < np * nterm; j += 32) sc[j] = w.coef[p0 * nterm + j];
+  for (int j = lane; j < np * nterm; j += 32) sc[j] = stage_coef<kMixed>(w.coef[p0 * nterm + j]);
   for (int j = lane; j < np; j += 32) s_c0[j] = w.c0[p0 + j];
   for (int q = 0; q < np; ++q) s_acc[q * 32 + lane] = 0.0;
   __syncwarp();
@@ -320,15 +361,38 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
       const double2* __restrict__ cq = sc + q * nterm;
       const double2* __restrict__ cr = cq + nterm;
       double a[N], b[N];
+      if constexpr (kMixed) {
+        // the two points' chains of one node share a packed FFMA2 pair
+        gna::f32x2 ab[N];
 #pragma unroll
-      for (int n = 0; n < N; ++n) a[n] = b[n] = 0.0;
-      GNA_UNROLL((NT ? NT : 1))
-      for (int j = 0; j < nterm; ++j) {
-        const double2 cw = cq[j], cv = cr[j];
+        for (int n = 0; n < N; ++n) ab[n] = 0ull;
+        GNA_UNROLL((NT ? NT : 1))
+        for (int j = 0; j < nterm; ++j) {
+          const double2 cw = cq[j], cv = cr[j];
+          const gna::f32x2 w2 = gna::f2_pack(__int_as_float(__double2loint(cw.y)),
+                                             __int_as_float(__double2loint(cv.y)));
+#pragma unroll
+          for (int n = 0; n < N; ++n) {
+            const gna::f32x2 h2 = gna::mixed_h2(cw.x, iE[n], cv.x, iE[n]);
+            ab[n] = gna::f2_fma(w2, gna::cos2_w2(h2), ab[n]);
+          }
+        }
 #pragma unroll
         for (int n = 0; n < N; ++n) {
-          a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
-          b[n] = fma(cv.y, gna::sin2c(cv.x, iE[n]), b[n]);
+          a[n] = (double)gna::f2_lo(ab[n]);
+          b[n] = (double)gna::f2_hi(ab[n]);
+        }
+      } else {
+#pragma unroll
+        for (int n = 0; n < N; ++n) a[n] = b[n] = 0.0;
+        GNA_UNROLL((NT ? NT : 1))
+        for (int j = 0; j < nterm; ++j) {
+          const double2 cw = cq[j], cv = cr[j];
+#pragma unroll
+          for (int n = 0; n < N; ++n) {
+            a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+            b[n] = fma(cv.y, gna::sin2c(cv.x, iE[n]), b[n]);
+          }
         }
       }
       double sa = s_acc[q * 32 + lane], sb = s_acc[(q + 1) * 32 + lane];
@@ -345,13 +409,28 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
     for (; q < np; ++q) {
       const double2* __restrict__ cq = sc + q * nterm;
       double a[N];
+      if constexpr (kMixed) {
+        float af[N];
 #pragma unroll
-      for (int n = 0; n < N; ++n) a[n] = 0.0;
-      GNA_UNROLL((NT ? NT : 1))
-      for (int j = 0; j < nterm; ++j) {
-        const double2 cw = cq[j];
+        for (int n = 0; n < N; ++n) af[n] = 0.0f;
+        GNA_UNROLL((NT ? NT : 1))
+        for (int j = 0; j < nterm; ++j) {
+          const double2 cw = cq[j];
+          const float wa = __int_as_float(__double2loint(cw.y));
 #pragma unroll
-        for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+          for (int n = 0; n < N; ++n) af[n] = fmaf(wa, gna::cos2_w(gna::mixed_h1(cw.x, iE[n])), af[n]);
+        }
+#pragma unroll
+        for (int n = 0; n < N; ++n) a[n] = (double)af[n];
+      } else {
+#pragma unroll
+        for (int n = 0; n < N; ++n) a[n] = 0.0;
+        GNA_UNROLL((NT ? NT : 1))
+        for (int j = 0; j < nterm; ++j) {
+          const double2 cw = cq[j];
+#pragma unroll
+          for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
+        }
       }
       double sv = s_acc[q * 32 + lane];
 #pragma unroll

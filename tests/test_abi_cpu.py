@@ -134,6 +134,9 @@ def _batch(lib, host=False, **kw):
             kw.get("data", 0x700000), kw.get("chi2", 0x800000)]
     if host:
         return lib.gna_oscprob_batch_host(*args, 0, None)
+    if "flags" in kw:
+        return lib.gna_oscprob_batch_ex(*args, kw.get("ws", 0x900000), kw.get("wsb", 1 << 20),
+                                        kw["flags"], None)
     return lib.gna_oscprob_batch(*args, kw.get("ws", 0x900000), kw.get("wsb", 1 << 20), None)
 
 
@@ -149,8 +152,27 @@ def _batch(lib, host=False, **kw):
 ])
 def test_batch_einval(lib, case):
     assert _batch(lib, **case) == gna.GNA_EINVAL
+    # the mixed tier (NEXT-3) validates exactly like the fp64 batch
+    assert _batch(lib, flags=gna.GNA_PREC_MIXED, **case) == gna.GNA_EINVAL
     if "ws" not in case and "wsb" not in case:
         assert _batch(lib, host=True, **case) == gna.GNA_EINVAL
+
+
+@pytest.mark.parametrize("flags", [8, 16 | 4, 1 | 2, 1 | 2 | 4, 0xffffffff])
+def test_batch_ex_bad_flags(lib, flags):
+    assert _batch(lib, flags=flags) == gna.GNA_EINVAL
+
+
+def test_header_constants_match_binding():
+    """The Python binding's constants are the header's #defines."""
+    src = open(HEADER).read()
+    for name in ("GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED", "GNA_MAX_ORDER",
+                 "GNA_MAX_NBASE", "GNA_OK", "GNA_EINVAL", "GNA_ECUDA", "GNA_ENODEV",
+                 "GNA_ENOMEM"):
+        m = (re.search(r"#define %s \(?(-?\d+)u?\)?" % name, src) or
+             re.search(r"\b%s = (-?\d+)" % name, src))  # enum gna_status
+        assert m, name
+        assert int(m.group(1)) == getattr(gna, name), name
 
 
 def _scan(lib, **kw):
@@ -294,6 +316,31 @@ def test_kernel_sin2_polynomial_accuracy(prefix, ncoef, bound):
             ref = mp.sin(mp.pi / 2 * (q + mp.mpf(float(f)))) ** 2
             worst = max(worst, abs(float(got - ref)))
     assert worst <= bound + 1.2e-16  # polynomial + final half-ulp of 1/2 +- v
+
+
+def test_mixed_tier_fp32_polynomial_accuracy():
+    """NEXT-3 mixed tier: -cos(pi y)/2 = W(h^2), y = 2m + 2h, with h rounded to fp32 (F2F, round
+    to nearest) and W evaluated by the kernel's fp32 FMA Horner chain (GNA_COS2F_*): within
+    1.3e-7 of the polynomial and 2.3e-7 of the exact value, for every residue class of y."""
+    src = open(os.path.join(_build.CSRC, "sin2_poly.h")).read()
+    cs = dict(re.findall(r"#define GNA_COS2F_C(\d) \(\(float\)([-0-9a-fx.p+]+)\)", src))
+    cf = [float.fromhex(cs[str(j)]) for j in range(len(cs))]
+    assert len(cf) == 7 and cf[0] == -0.5
+    f32 = lambda x: float(np.float32(x))  # noqa: E731
+    mp.mp.dps = 30
+    g = np.random.default_rng(8)
+    worst_poly = worst = 0.0
+    for h in np.r_[np.linspace(-0.5, 0.5, 601), g.uniform(-0.5, 0.5, 300)]:
+        hs = f32(h)
+        u = f32(Fraction(hs) * Fraction(hs))
+        p = cf[-1]
+        for c in reversed(cf[:-1]):
+            p = f32(Fraction(p) * Fraction(u) + Fraction(c))
+        worst_poly = max(worst_poly, abs(p - float(-mp.cos(2 * mp.pi * mp.mpf(hs)) / 2)))
+        for m in (0, 1, 37):  # y = 2m + 2h: the value does not depend on m
+            ref = -mp.cos(mp.pi * (2 * m + 2 * mp.mpf(float(h)))) / 2
+            worst = max(worst, abs(p - float(ref)))
+    assert worst_poly <= 1.3e-7 and worst <= 2.3e-7
 
 
 def test_kernel_sin2_small_phase_error_vanishes():

@@ -308,9 +308,10 @@ def _batch_case(g, P, nbase, nbins, order):
     return pts, L, om, edges, data
 
 
-def _run_batch(gna, pts, L, om, edges, order, data, spectra=True):
+def _run_batch(gna, pts, L, om, edges, order, data, spectra=True, precision="fp64"):
     sp, x2 = gna.oscprob_batch({k: _t(v) for k, v in pts.items()}, L, om, _t(edges), order,
-                               data=_t(data) if data is not None else None, spectra=spectra)
+                               data=_t(data) if data is not None else None, spectra=spectra,
+                               precision=precision)
     return (_np(sp) if sp is not None else None), (_np(x2) if x2 is not None else None)
 
 
@@ -340,6 +341,61 @@ def test_batch_points_inner_path_vs_oracle(gna, order):
     spr, x2r = oracle.batch(pts, L, om, edges, order, data=data, nthreads=_nt())
     assert np.max(np.abs(sp - spr) / np.abs(spr)) <= TOL_BIN
     assert np.all(np.abs(x2 - x2r) <= _chi2_bound(spr, data))
+
+
+# ------------------------------------------------------------------------ NEXT-3 mixed tier
+# fp64 phases/reduction, fp32 polynomial and per-node term sums (GNA_PREC_MIXED).  Tier
+# tolerance: 1e-5 relative on spectra; chi^2 within the bound it propagates.
+TOL_MIXED = 1e-5
+
+
+def _chi2_bound_tol(T, D, tol):
+    d = np.abs(T - D)
+    return np.sum((2 * d * tol * np.abs(T) + (tol * T) ** 2) / D, axis=-1) + 1e-300
+
+
+@pytest.mark.parametrize("P,nbase,nbins,order", [
+    (7, 3, 37, 4), (1, 1, 1, 1), (3, 2, 128, 10), (5, 8, 129, 10), (2, 64, 50, 32),
+    (33, 1, 300, 5), (40, 1, 1000, 10)])
+def test_batch_mixed_vs_oracle(gna, P, nbase, nbins, order):
+    g = synth.rng(900 + P * nbase + nbins)
+    pts, L, om, edges, data = _batch_case(g, P, nbase, nbins, order)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data, precision="mixed")
+    spr, x2r = oracle.batch(pts, L, om, edges, order, data=data, nthreads=_nt())
+    err = np.max(np.abs(sp - spr) / np.abs(spr))
+    assert err <= TOL_MIXED
+    assert np.all(np.abs(x2 - x2r) <= _chi2_bound_tol(spr, data, TOL_MIXED))
+    # it really is the fp32 path (the fp64 path is ~1e-15 from the oracle)
+    sp64, _ = _run_batch(gna, pts, L, om, edges, order, data)
+    assert np.max(np.abs(sp64 - spr) / np.abs(spr)) <= TOL_BIN
+    if nbins * order >= 10:
+        assert np.max(np.abs(sp - sp64)) > 0
+    # chi2-only and spectra-only runs give the same bits
+    sp2, _ = _run_batch(gna, pts, L, om, edges, order, None, precision="mixed")
+    _, x22 = _run_batch(gna, pts, L, om, edges, order, data, spectra=False, precision="mixed")
+    assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
+
+
+@pytest.mark.parametrize("cfg,idx", [("cfg5", [0, 417, 999]), ("cfg4", [0, 1, 5000, 9999])])
+def test_batch_mixed_full_size_sampled_and_split_invariant(gna, cfg, idx):
+    """The mixed tier at the bench launch configuration (cfg5: per-point kernel; cfg4:
+    points-inner kernel): sampled parity at the tier tolerance, and a point's result does not
+    depend on the other points of the call (bitwise), as for the fp64 path."""
+    c = synth.config(cfg)
+    sp, x2 = _run_batch(gna, c["points"], c["L_km"], c["omega"], c["edges"], c["order"],
+                        c["data"], precision="mixed")
+    idx = np.array(idx)
+    sub = synth.subset_points(c["points"], idx)
+    spr, x2r = oracle.batch(sub, c["L_km"], c["omega"], c["edges"], c["order"], data=c["data"],
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_MIXED
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound_tol(spr, c["data"], TOL_MIXED))
+    n = sp.shape[0]
+    for lo, hi in ((0, n // 7), (n // 7, n)):
+        s2 = synth.subset_points(c["points"], np.arange(lo, hi))
+        sps, x2s = _run_batch(gna, s2, c["L_km"], c["omega"], c["edges"], c["order"], c["data"],
+                              precision="mixed")
+        assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi])
 
 
 def test_batch_single_baseline_matches_gl_integrate(gna):

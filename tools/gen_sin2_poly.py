@@ -123,6 +123,26 @@ def horner_fp64(cf, u):
     return p
 
 
+def r32(x) -> float:
+    """Nearest fp32 value (as a Python float) of a float or Fraction."""
+    import numpy as np
+    return float(np.float32(float(x)))
+
+
+def max_err_fp32(cf, npts=4000):
+    """Mixed tier (NEXT-3): the reduced argument rounded to fp32, u = f*f and the Horner chain
+    in fp32 FMA (error against the current V at the rounded argument)."""
+    worst = 0.0
+    for i in range(npts + 1):
+        f = r32(0.5 * i / npts)
+        u = r32(Fraction(f) * Fraction(f))
+        p = cf[-1]
+        for c in reversed(cf[:-1]):
+            p = r32(Fraction(p) * Fraction(u) + Fraction(c))
+        worst = max(worst, abs(float(p - V(mp.mpf(f) ** 2))))
+    return worst
+
+
 def max_err(cf, npts=4000):
     worst = 0.0
     for i in range(npts + 1):
@@ -189,6 +209,18 @@ def main():
     cf7 = [float(x) for x in remez_c0(7)]
     err7 = max_err(cf7)
     print("degree 7 (c0 = -1/2 pinned) max |err| fp64 Horner:", err7, file=sys.stderr)
+    # full-period form for the packed (FFMA2) mixed kernels: reducing y modulo 2,
+    # y = 2m + 2h with |h| <= 1/2, gives (-1)^q v(f) = -cos(pi y)/2 = -cos(2 pi h)/2 with no
+    # sign flip; W(u) = -cos(2 pi sqrt u)/2 on u = h^2 in [0, 1/4], degree 6 in fp32
+    global V
+    V0 = V
+    V = lambda u: -mp.cos(2 * mp.pi * mp.sqrt(u)) / 2  # noqa: E731
+    try:
+        cfw = [r32(x) for x in remez_c0(6)]
+        errw = max_err_fp32(cfw)
+    finally:
+        V = V0
+    print("fp32 full-period degree 6 max |err| fp32 Horner:", errw, file=sys.stderr)
     lines = [
         "// GENERATED by tools/gen_sin2_poly.py — do not edit.",
         "// v(u) = -cos(pi*sqrt(u))/2 on u in [0, 1/4] (u = f^2, |f| <= 1/2), minimax.",
@@ -203,6 +235,12 @@ def main():
         lines.append("#define GNA_SIN2_C%d (%s)  /* %.17g */" % (j, x.hex(), x))
     for j, x in enumerate(cf7):
         lines.append("#define GNA_SIN2_D7_C%d (%s)  /* %.17g */" % (j, x.hex(), x))
+    lines.append("// Mixed tier (NEXT-3): W(u) = -cos(2 pi sqrt(u))/2 on u = h^2 in [0, 1/4] (y reduced")
+    lines.append("// modulo 2, no sign flip), fp32 degree 6, c0 = -1/2 pinned; max abs error with h rounded")
+    lines.append("// to fp32 and an fp32 FMA Horner chain: %.3e." % errw)
+    lines.append("#define GNA_COS2F_ERR %.3e" % errw)
+    for j, x in enumerate(cfw):
+        lines.append("#define GNA_COS2F_C%d ((float)%s)  /* %.9g */" % (j, x.hex(), x))
     open(out, "w").write("\n".join(lines) + "\n")
     print("wrote", out, "err", err, file=sys.stderr)
 

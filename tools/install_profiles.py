@@ -37,6 +37,7 @@ CAPTURES = {
     "eval_ab": ("cfg3emu", "k_oscprob_eval_tma<PabCoef>"),
     "gl": ("cfg2", "k_gl_integrate"),
     "scan": ("cfg4grid", "k_scan_expand"),
+    "batch_mixed": ("cfg5_mixed", "k_oscprob_batch<..., kMixed>"),
 }
 
 
@@ -86,6 +87,14 @@ def main():
         with open(os.path.join(prof, "%s_bench_%s.jsonl" % (R, w)), "w") as f:
             f.write(json.dumps(d) + "\n")
         print("bench", w, "%.4g" % d["value"], d["unit"])
+    for w in ("cfg5", "cfg4"):
+        p = os.path.join(src, "bench_%s_mixed.log" % w)
+        if os.path.exists(p):
+            d = last_json(p)
+            units[w + "_mixed"] = d["config"].get("energy_points_per_step")
+            with open(os.path.join(prof, "%s_bench_%s_mixed.jsonl" % (R, w)), "w") as f:
+                f.write(json.dumps(d) + "\n")
+            print("bench", w, "mixed", "%.4g" % d["value"])
     p = os.path.join(src, "bench_reference.log")
     if os.path.exists(p):
         with open(os.path.join(prof, "%s_bench_reference_cfg5.jsonl" % R), "w") as f:

@@ -13,6 +13,7 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "base": dict(),
+    "mx_magic": dict(GNA_MIXED_CVT=1),
     "d7_mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
     "d7_mb18": dict(GNA_BATCH_MINB=18, GNA_BATCH_PI_MINB=1),
     "d7_ju2": dict(GNA_BATCH_JUNROLL=2),
@@ -39,8 +40,9 @@ VARIANTS = {
 }
 
 
-KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0E",
-           r"k_oscprob_batch_piILi5ELi0ELi0E", r"k_oscprob_batch_piILi5ELi0ELi3E"]
+KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb0E",
+           r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
+           r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E"]
 
 
 def main(names):
