@@ -262,7 +262,8 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
  * asynchronous memory copying").  Same arithmetic as the device entry points
  * (bitwise identical results); inputs are copied host->device and results
  * device->host in chunks so that the copies overlap the kernels.  chunk = 0
- * picks a default.  Returns after the results are in host memory.
+ * picks a default (batch: ~8 MiB of spectra per chunk, or a single chunk when
+ * only chi^2 is requested).  Returns after the results are in host memory.
  * ------------------------------------------------------------------------- */
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
                           double* h_P, int64_t chunk, void* stream);

@@ -763,8 +763,10 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   if ((rc = stage_init(S))) return rc;
   const int64_t P = h_pts->npoints;
   if (chunk_points <= 0) {
-    // ~8 MiB of spectra per chunk, at least 1 point
-    chunk_points = ((int64_t)8 << 20) / (nbins * 8);
+    // ~8 MiB of spectra per chunk (their D2H overlaps the next chunk's kernels), at least 1
+    // point; without spectra there is nothing large to overlap: one launch over all points
+    // (chunking would only add per-chunk launches and partial last waves)
+    chunk_points = h_spectra ? ((int64_t)8 << 20) / (nbins * 8) : P;
     if (chunk_points < 1) chunk_points = 1;
   }
   if (chunk_points > P) chunk_points = P;
