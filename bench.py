@@ -678,7 +678,7 @@ def main():
     if tr:
         roof["traffic"] = tr["bytes"]
         roof["traffic_source"] = tr["source"]
-        roof["algorithmic_bytes"] = tr["algorithmic_bytes"]
+        roof["algorithmic_bytes"] = tr.get("algorithmic_bytes")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if scaling == "strong" else "weak",

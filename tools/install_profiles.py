@@ -132,6 +132,8 @@ def main():
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         b = int(rd * scale.get(unit_r, 1) + wr * scale.get(unit_w, 1))
         ent = traffic.get(w, {})
+        if "algorithmic_bytes" not in ent and w.endswith("_mixed"):
+            ent["algorithmic_bytes"] = traffic.get(w[:-len("_mixed")], {}).get("algorithmic_bytes")
         ent.update(kernel=label, bytes=b,
                    source="profiles/%s_final_ncu_%s_summary.txt" % (R, name))
         traffic[w] = ent

@@ -4,6 +4,7 @@
 set -u
 R=${ROUND:-r01}
 mkdir -p gpurun_out/final
+if [ -z "${PROF_ONLY:-}" ]; then
 for w in cfg5 cfg4 cfg3 cfg2 cfg1 cfg4grid cfg3emu cfg5fit; do
   timeout 400 python bench.py --workload $w > gpurun_out/final/bench_$w.log 2>&1; echo "$w rc=$?"
 done
@@ -17,8 +18,10 @@ timeout 400 $D > gpurun_out/final/plain_default.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/final/launches_default.csv $D > gpurun_out/final/ncu_launch.log 2>&1
 echo "launches rc=$?"
-prof() {  # name workload kernel-regex [extra bench args]
-  local B="python bench.py --workload $2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --graph off $4"
+fi
+prof() {  # name workload kernel-regex [extra bench args]; PROFS="a b" limits the set
+  case " ${PROFS:-$1} " in *" $1 "*) ;; *) return 0 ;; esac
+  local B="python bench.py --workload $2 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --graph off ${4:-}"
   timeout 300 $B > gpurun_out/final/plain_$1.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:$3 -s 3 -c 1 \
         -o gpurun_out/final/prof_$1 $B > gpurun_out/final/ncu_$1.log 2>&1
