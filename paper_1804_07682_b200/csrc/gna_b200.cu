@@ -266,6 +266,10 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut, kMixed>
               : (order % 3 == 0) ? k_oscprob_batch<kBatchWarps, 3, kOut, kMixed>
                                  : k_oscprob_batch<kBatchWarps, 4, kOut, kMixed>;
+#if GNA_MIXED_N10
+  // mixed tier: 10 nodes (5 packed pairs) per coefficient load when the order allows
+  if (kMixed && order % 10 == 0) kern = k_oscprob_batch<kBatchWarps, 10, kOut, kMixed>;
+#endif
   if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
     // several points per warp: node groups outer, points inner (bitwise-identical sums)
     ppw = std::min<int64_t>(ppw, kMaxPPW);

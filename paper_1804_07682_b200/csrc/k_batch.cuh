@@ -119,6 +119,12 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_MINB
 #define GNA_BATCH_MINB 1
 #endif
+#ifndef GNA_MIXED_N10
+#define GNA_MIXED_N10 1
+#endif
+#ifndef GNA_MIXED_JUNROLL
+#define GNA_MIXED_JUNROLL 1
+#endif
 #ifndef GNA_BATCH_PI_NT
 #define GNA_BATCH_PI_NT 1
 #endif
@@ -151,7 +157,7 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     float acc1 = 0.0f;
 #pragma unroll
     for (int k = 0; k < NP; ++k) acc2[k] = 0ull;
-    GNA_UNROLL(GNA_BATCH_JUNROLL)
+    GNA_UNROLL(GNA_MIXED_JUNROLL)
     for (int j = 0; j < nterm; ++j) {
       const double2 cw = sc[j];
       const gna::f32x2 w2 = (gna::f32x2)__double_as_longlong(cw.y);

@@ -14,6 +14,16 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 VARIANTS = {
     "base": dict(),
     "mx_magic": dict(GNA_MIXED_CVT=1),
+    "mx_ju1": dict(GNA_MIXED_JUNROLL=1),
+    "mx_n10": dict(GNA_MIXED_N10=1),
+    "mx_n5": dict(GNA_MIXED_N10=0, GNA_MIXED_JUNROLL=2),
+    "mx_n10_ju2": dict(GNA_MIXED_JUNROLL=2),
+    "mx_n10_magic": dict(GNA_MIXED_CVT=1),
+    "mx_n10_ju1": dict(GNA_MIXED_N10=1, GNA_MIXED_JUNROLL=1),
+    "mx_ju3": dict(GNA_MIXED_JUNROLL=3),
+    "mx_ju4": dict(GNA_MIXED_JUNROLL=4),
+    "mx_mb16": dict(GNA_BATCH_MINB=16, GNA_BATCH_PI_MINB=1),
+    "mx_mb24": dict(GNA_BATCH_MINB=24, GNA_BATCH_PI_MINB=1),
     "d7_mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
     "d7_mb18": dict(GNA_BATCH_MINB=18, GNA_BATCH_PI_MINB=1),
     "d7_ju2": dict(GNA_BATCH_JUNROLL=2),
@@ -42,7 +52,8 @@ VARIANTS = {
 
 KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb0E",
            r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
-           r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E"]
+           r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E",
+           r"k_oscprob_batchILi1ELi10ELi0ELb1E"]
 
 
 def main(names):
