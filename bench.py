@@ -337,8 +337,33 @@ def cpu_baseline(c, name, seconds):
         dt = time.perf_counter() - t0
         units = n
         sample = "%d of %d energies of cfg3 (same linspace range)" % (n, c["n"])
-    return {"value": units / dt, "unit": UNIT, "cores": nt, "kind": "oracle",
-            "sample": sample, "seconds": dt}
+    out = {"value": units / dt, "unit": UNIT, "cores": nt, "kind": "oracle",
+           "sample": sample, "seconds": dt, "cpu_model": _cpu_model()}
+    # the oracle at 1 thread as well as on all cores (bounded sample)
+    if name in ("cfg4", "cfg5", "cfg4grid"):
+        t0 = time.perf_counter()
+        oracle.batch(synth.subset_points(c["points"], np.arange(1)), c["L_km"], c["omega"],
+                     c["edges"], c["order"], data=c["data"], nthreads=1)
+        dt1 = time.perf_counter() - t0
+        out["single_thread"] = {"value": per_point / dt1, "sample": "1 parameter point of %s" % name}
+    elif name in ("cfg2", "cfg3", "cfg3emu"):
+        E = np.linspace(1.0, 10.0, 2_000_000)
+        ab = (0, 1) if name == "cfg3emu" else (0, 0)
+        t0 = time.perf_counter()
+        oracle.prob_array(c["params"], c["L_km"], E, alpha=ab[0], beta=ab[1], nthreads=1)
+        dt1 = time.perf_counter() - t0
+        out["single_thread"] = {"value": E.size / dt1, "sample": "2e6 energies, 1 thread"}
+    return out
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ----------------------------------------------------------------------------- our arm
