@@ -288,7 +288,7 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
 #if GNA_BATCH_PI_TAIL
     // Few waves (e.g. cfg4: ~8): pick the points per warp in [ppw/2, ppw] that minimises
     // waves x (ppw + per-block overhead), so the last wave is not mostly idle
-    // (DESIGN.md §6.3).  The grouping never changes a point's result.
+    // (DESIGN.md §6.2).  The grouping never changes a point's result.
     {
       const int64_t hi = ppw;
       double best = 0.0;

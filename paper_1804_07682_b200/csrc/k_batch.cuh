@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     }
     __syncwarp();
     // bin = sum_n h w_n (c0 - a_n) = c0 W - A,  W = sum_n h w_n,  A = sum_n h w_n a_n
-    // (one FP64 op per node instead of two; DESIGN.md §6.3)
+    // (one FP64 op per node instead of two; DESIGN.md §6.2)
     double W = 0.0, A = 0.0;
     int i = 0;
     for (; i + N <= order; i += N) batch_nodes<N, kMixed>(sc, nterm, invE, hw, nbins, i, W, A);
