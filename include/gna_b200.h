@@ -203,6 +203,21 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
                          void* stream);
 
 /* ---------------------------------------------------------------------------
+ * gna_oscprob_eval_ex / gna_gl_integrate_ex — gna_oscprob_eval / gna_gl_integrate
+ * with flags: 0 = the same call; GNA_PREC_MIXED = the mixed-precision tier above
+ * (fp64 phase and modulo-2 reduction, fp32 polynomial and term sum, two energies or
+ * GL nodes per packed FP32 FMA).  Tier tolerance: 1e-6 absolute on P, 1e-5
+ * relative on bin integrals.  Any other flag bit: GNA_EINVAL.
+ * Arguments, layouts and other errors as the fp64 calls.
+ * ------------------------------------------------------------------------- */
+int gna_oscprob_eval_ex(const gna_osc_params* p, double L_km, const double* d_E, int64_t n,
+                        double* d_P, uint32_t flags, void* stream);
+
+int gna_gl_integrate_ex(const gna_osc_params* p, double L_km, const double* d_edges,
+                        int64_t nbins, int32_t order, double* d_bins, uint32_t flags,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------
  * gna_fit_pattern_search — NEXT-4 (second part): a chi^2 minimiser that stays on the
  * GPU (the minimisation of P:446-451), driving the batch kernels.  Deterministic
  * compass search over x = (theta12, theta13, dm2_21, dm2_31): each iteration

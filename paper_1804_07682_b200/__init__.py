@@ -40,7 +40,7 @@ EXPORTS = (
     "gna_oscprob_batch", "gna_oscprob_eval_host", "gna_gl_integrate_host",
     "gna_oscprob_batch_host", "gna_release",
     "gna_gl_rule", "gna_strerror", "gna_last_cuda_error", "gna_abi_version", "gna_launch_count",
-    "gna_sin2_poly_degree",
+    "gna_sin2_poly_degree", "gna_oscprob_eval_ex", "gna_gl_integrate_ex",
     "gna_oscprob_scan_workspace_size", "gna_oscprob_scan", "gna_oscprob_eval_ab",
     "gna_oscprob_batch_ex", "gna_gl_integrate_ab", "gna_fit_workspace_size",
     "gna_fit_pattern_search",
@@ -122,6 +122,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
     B = ctypes.POINTER(_CBatch)
     L.gna_oscprob_eval.argtypes = [P, d, vp, i64, vp, vp]
     L.gna_gl_integrate.argtypes = [P, d, vp, i64, i32, vp, vp]
+    L.gna_oscprob_eval_ex.argtypes = [P, d, vp, i64, vp, ctypes.c_uint32, vp]
+    L.gna_gl_integrate_ex.argtypes = [P, d, vp, i64, i32, vp, ctypes.c_uint32, vp]
+    L.gna_oscprob_eval_ex.restype = ctypes.c_int
+    L.gna_gl_integrate_ex.restype = ctypes.c_int
     L.gna_oscprob_eval_ab.argtypes = [i32, i32, P, d, vp, i64, vp, vp]
     L.gna_oscprob_batch_ex.argtypes = [B, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, sz,
                                        ctypes.c_uint32, vp]
@@ -202,16 +206,29 @@ def _small(a, name) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- device entry points
-def oscprob_eval(params, L_km: float, E, out=None, stream=None):
-    """P_ee over a device energy tensor (gna_oscprob_eval)."""
+def _prec_flags(precision: str) -> int:
+    if precision not in ("fp64", "mixed"):
+        raise ValueError("precision must be 'fp64' or 'mixed'")
+    return GNA_PREC_MIXED if precision == "mixed" else 0
+
+
+def oscprob_eval(params, L_km: float, E, out=None, stream=None, precision: str = "fp64"):
+    """P_ee over a device energy tensor (gna_oscprob_eval; precision="mixed":
+    gna_oscprob_eval_ex with GNA_PREC_MIXED, the NEXT-3 1e-6 tier)."""
     import torch
     L = load()
     n = E.numel()
+    flags = _prec_flags(precision)
     if out is None:
         out = torch.empty_like(E)
     p = OscParams.of(params)._c()
-    _check(L.gna_oscprob_eval(ctypes.byref(p), float(L_km), _dev(E, "E"), n,
-                              _dev(out, "out", n), _stream(stream)), "gna_oscprob_eval")
+    if flags:
+        _check(L.gna_oscprob_eval_ex(ctypes.byref(p), float(L_km), _dev(E, "E"), n,
+                                     _dev(out, "out", n), flags, _stream(stream)),
+               "gna_oscprob_eval_ex")
+    else:
+        _check(L.gna_oscprob_eval(ctypes.byref(p), float(L_km), _dev(E, "E"), n,
+                                  _dev(out, "out", n), _stream(stream)), "gna_oscprob_eval")
     return out
 
 
@@ -246,17 +263,23 @@ def gl_integrate_ab(alpha: int, beta: int, params, L_km: float, edges, order: in
     return out
 
 
-def gl_integrate(params, L_km: float, edges, order: int, out=None, stream=None):
-    """Per-bin Gauss-Legendre integrals of P_ee (gna_gl_integrate)."""
+def gl_integrate(params, L_km: float, edges, order: int, out=None, stream=None,
+                 precision: str = "fp64"):
+    """Per-bin Gauss-Legendre integrals of P_ee (gna_gl_integrate; precision="mixed":
+    gna_gl_integrate_ex with GNA_PREC_MIXED, the NEXT-3 1e-5 tier)."""
     import torch
     L = load()
     nbins = edges.numel() - 1
+    flags = _prec_flags(precision)
     if out is None:
         out = torch.empty(max(nbins, 0), dtype=torch.float64, device=edges.device)
     p = OscParams.of(params)._c()
-    _check(L.gna_gl_integrate(ctypes.byref(p), float(L_km), _dev(edges, "edges"), nbins,
-                              int(order), _dev(out, "out", max(nbins, 0)), _stream(stream)),
-           "gna_gl_integrate")
+    args = (ctypes.byref(p), float(L_km), _dev(edges, "edges"), nbins, int(order),
+            _dev(out, "out", max(nbins, 0)))
+    if flags:
+        _check(L.gna_gl_integrate_ex(*args, flags, _stream(stream)), "gna_gl_integrate_ex")
+    else:
+        _check(L.gna_gl_integrate(*args, _stream(stream)), "gna_gl_integrate")
     return out
 
 
@@ -273,11 +296,10 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
     spectra: True to allocate, a [P, nbins] tensor to fill, or None/False.
     chi2: computed when `data` is given (a [P] tensor may be passed to fill).
     precision: "fp64" (gna_oscprob_batch, the 1e-11 tier) or "mixed" (gna_oscprob_batch_ex
-    with GNA_PREC_MIXED: fp64 phases, fp32 polynomial and term sums; 1e-6 tier).
+    with GNA_PREC_MIXED: fp64 phases, fp32 polynomial and term sums; 1e-5 tier).
     Returns (spectra or None, chi2 or None).
     """
-    if precision not in ("fp64", "mixed"):
-        raise ValueError("precision must be 'fp64' or 'mixed'")
+    _prec_flags(precision)
     import torch
     L = load()
     P = points["theta12"].numel()

@@ -98,6 +98,17 @@ void make_coef(const gna_osc_params* p, double L_km, PeeCoef* c) {
   c->c0 = 1.0 - 0.5 * ((w21 + w31) + w32);
 }
 
+// NEXT-3 mixed tier: the same coefficients with kq halved (exact) and the weights in fp32
+void make_coef_mix(const gna_osc_params* p, double L_km, gna::PeeMixCoef* c) {
+  PeeCoef d;
+  make_coef(p, L_km, &d);
+  for (int j = 0; j < 3; ++j) {
+    c->kqh[j] = 0.5 * d.kq[j];
+    c->w[j] = (float)d.w[j];
+  }
+  c->c0 = d.c0;
+}
+
 // NEXT-2: coefficients of any channel alpha -> beta.  PMNS elements from the PDG
 // closed form (independent of the oracle's matrix product), conj for antineutrinos
 // (S:256); X_ij = V*_ai V_bi V_aj V*_bj for pairs (2,1), (3,1), (3,2).
@@ -476,6 +487,19 @@ int gna_oscprob_eval(const gna_osc_params* p, double L_km, const double* d_E, in
   return launch_eval(c, d_E, n, d_P, (cudaStream_t)stream);
 }
 
+int gna_oscprob_eval_ex(const gna_osc_params* p, double L_km, const double* d_E, int64_t n,
+                        double* d_P, uint32_t flags, void* stream) {
+  if (flags & ~GNA_PREC_MIXED) return GNA_EINVAL;
+  if (!flags) return gna_oscprob_eval(p, L_km, d_E, n, d_P, stream);
+  int rc = validate_eval(p, L_km, d_E, n, d_P);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_E) || check_dev_ptr(d_P)) return GNA_EINVAL;
+  gna::PeeMixCoef c;
+  make_coef_mix(p, L_km, &c);
+  return launch_eval(c, d_E, n, d_P, (cudaStream_t)stream);
+}
+
 int gna_oscprob_eval_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, double L_km,
                         const double* d_E, int64_t n, double* d_P, void* stream) {
   if (alpha < 0 || alpha > 2 || beta < 0 || beta > 2) return GNA_EINVAL;
@@ -496,6 +520,19 @@ int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges
   if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
   PeeCoef c;
   make_coef(p, L_km, &c);
+  return launch_gl(c, d_edges, nbins, order, d_bins, (cudaStream_t)stream);
+}
+
+int gna_gl_integrate_ex(const gna_osc_params* p, double L_km, const double* d_edges, int64_t nbins,
+                        int32_t order, double* d_bins, uint32_t flags, void* stream) {
+  if (flags & ~GNA_PREC_MIXED) return GNA_EINVAL;
+  if (!flags) return gna_gl_integrate(p, L_km, d_edges, nbins, order, d_bins, stream);
+  int rc = validate_gl(p, L_km, d_edges, nbins, order, d_bins);
+  if (rc) return rc;
+  if ((rc = check_device())) return rc;
+  if (check_dev_ptr(d_edges) || check_dev_ptr(d_bins)) return GNA_EINVAL;
+  gna::PeeMixCoef c;
+  make_coef_mix(p, L_km, &c);
   return launch_gl(c, d_edges, nbins, order, d_bins, (cudaStream_t)stream);
 }
 

@@ -242,6 +242,30 @@ __device__ __forceinline__ double pee_inv(const PeeCoef& c, double invE) {
   return c.c0 - acc;
 }
 
+// NEXT-3 mixed tier of the single-point paths (eval, GL): phase slopes halved (modulo-2
+// reduction, see mixed_h), weights in fp32, the term sum of one energy in fp32.
+struct PeeMixCoef {
+  double kqh[3];  // kq / 2
+  float w[3];
+  double c0;
+};
+
+__device__ __forceinline__ double prob_inv(const PeeMixCoef& c, double invE) {
+  float acc = c.w[0] * cos2_w(mixed_h1(c.kqh[0], invE));
+  acc = fmaf(c.w[1], cos2_w(mixed_h1(c.kqh[1], invE)), acc);
+  acc = fmaf(c.w[2], cos2_w(mixed_h1(c.kqh[2], invE)), acc);
+  return c.c0 - (double)acc;
+}
+
+// two energies per packed FFMA2 chain (the elementwise kernels' double2 pairs)
+__device__ __forceinline__ double2 prob_pair(const PeeMixCoef& c, double iE0, double iE1) {
+  f32x2 acc = 0ull;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+    acc = f2_fma(f2_pack(c.w[j], c.w[j]), cos2_w2(mixed_h2(c.kqh[j], iE0, c.kqh[j], iE1)), acc);
+  return make_double2(c.c0 - (double)f2_lo(acc), c.c0 - (double)f2_hi(acc));
+}
+
 // Any channel alpha -> beta (NEXT-2): P = c0 + sum_ij (-1)^q (a_ij v + b_ij sin(pi f)),
 // c0 = delta_ab + sum_ij a_ij / 2.
 struct PabCoef {
@@ -261,6 +285,12 @@ __device__ __forceinline__ double pab_inv(const PabCoef& c, double invE) {
 __device__ __forceinline__ double prob_inv(const PeeCoef& c, double invE) { return pee_inv(c, invE); }
 __device__ __forceinline__ double prob_inv(const PabCoef& c, double invE) { return pab_inv(c, invE); }
 
+// a pair of energies (the elementwise kernels' double2): two independent evaluations
+template <class Coef>
+__device__ __forceinline__ double2 prob_pair(const Coef& c, double iE0, double iE1) {
+  return make_double2(prob_inv(c, iE0), prob_inv(c, iE1));
+}
+
 // H energies at once, term-major: every coefficient feeds H independent chains (ILP = H).
 // The term loop is deliberately not unrolled: one basic block per term keeps ptxas from
 // serialising the H chains to save registers (it does so in fully unrolled straight-line
@@ -279,6 +309,31 @@ __device__ __forceinline__ void prob_inv_n(const PeeCoef& c, const double (&iE)[
   }
 #pragma unroll
   for (int i = 0; i < H; ++i) P[i] = c.c0 - acc[i];
+}
+
+template <int H>
+__device__ __forceinline__ void prob_inv_n(const PeeMixCoef& c, const double (&iE)[H],
+                                           double (&P)[H]) {
+  constexpr int NP = H / 2;
+  f32x2 acc2[NP > 0 ? NP : 1];
+  float acc1 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) acc2[k] = 0ull;
+#pragma unroll 1
+  for (int j = 0; j < 3; ++j) {
+    const double kqh = j == 0 ? c.kqh[0] : (j == 1 ? c.kqh[1] : c.kqh[2]);
+    const float w = j == 0 ? c.w[0] : (j == 1 ? c.w[1] : c.w[2]);
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      acc2[k] = f2_fma(f2_pack(w, w), cos2_w2(mixed_h2(kqh, iE[2 * k], kqh, iE[2 * k + 1])), acc2[k]);
+    if constexpr (H & 1) acc1 = fmaf(w, cos2_w(mixed_h1(kqh, iE[H - 1])), acc1);
+  }
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    P[2 * k] = c.c0 - (double)f2_lo(acc2[k]);
+    P[2 * k + 1] = c.c0 - (double)f2_hi(acc2[k]);
+  }
+  if constexpr (H & 1) P[H - 1] = c.c0 - (double)acc1;
 }
 
 template <int H>

@@ -18,9 +18,7 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(Coef c,
     double2* __restrict__ P2 = reinterpret_cast<double2*>(P);
     for (int64_t i = tid; i < n2; i += stride) {
       const double2 e = __ldcs(E2 + i);
-      double2 r;
-      r.x = gna::prob_inv(c, gna::rcp(e.x));
-      r.y = gna::prob_inv(c, gna::rcp(e.y));
+      const double2 r = gna::prob_pair(c, gna::rcp(e.x), gna::rcp(e.y));
       __stcs(P2 + i, r);
     }
     if ((n & 1) && tid == 0) P[n - 1] = gna::prob_inv(c, gna::rcp(E[n - 1]));
@@ -86,9 +84,7 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
 #pragma unroll
     for (int j = threadIdx.x; j < kEvalTile / 2; j += kEvalTmaThreads) {
       const double2 e = buf[j];
-      double2 r;
-      r.x = gna::prob_inv(c, gna::rcp(e.x));
-      r.y = gna::prob_inv(c, gna::rcp(e.y));
+      const double2 r = gna::prob_pair(c, gna::rcp(e.x), gna::rcp(e.y));
       buf[j] = r;
     }
     gna::fence_proxy_async_smem();
@@ -111,9 +107,7 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
 #pragma unroll
     for (int j = threadIdx.x; j < kEvalTile / 2; j += kEvalTmaThreads) {
       const double2 e = src[j];
-      double2 r;
-      r.x = gna::prob_inv(c, gna::rcp(e.x));
-      r.y = gna::prob_inv(c, gna::rcp(e.y));
+      const double2 r = gna::prob_pair(c, gna::rcp(e.x), gna::rcp(e.y));
       __stcs(dst + j, r);
     }
     __syncthreads();  // every thread is done with stage st before it is refilled

@@ -163,6 +163,23 @@ def test_batch_ex_bad_flags(lib, flags):
     assert _batch(lib, flags=flags) == gna.GNA_EINVAL
 
 
+@pytest.mark.parametrize("flags", [1, 2, 8, 1 | 4, 0xffffffff])
+def test_eval_gl_ex_bad_flags(lib, flags):
+    """The single-point _ex calls accept only GNA_PREC_MIXED (NEXT-3)."""
+    assert lib.gna_oscprob_eval_ex(_params(), 1.0, BAD, 10, BAD2, flags, None) == gna.GNA_EINVAL
+    assert lib.gna_gl_integrate_ex(_params(), 1.0, BAD, 10, 5, BAD2, flags,
+                                   None) == gna.GNA_EINVAL
+
+
+def test_eval_gl_ex_mixed_validates_like_fp64(lib):
+    m = gna.GNA_PREC_MIXED
+    assert lib.gna_oscprob_eval_ex(_params(), -1.0, BAD, 10, BAD2, m, None) == gna.GNA_EINVAL
+    assert lib.gna_oscprob_eval_ex(_params(), 1.0, BAD, 0, BAD2, m, None) == gna.GNA_EINVAL
+    assert lib.gna_oscprob_eval_ex(None, 1.0, BAD, 10, BAD2, m, None) == gna.GNA_EINVAL
+    assert lib.gna_gl_integrate_ex(_params(), 1.0, BAD, 10, 33, BAD2, m, None) == gna.GNA_EINVAL
+    assert lib.gna_gl_integrate_ex(_params(), 1.0, BAD, 0, 5, BAD2, m, None) == gna.GNA_EINVAL
+
+
 def test_header_constants_match_binding():
     """The Python binding's constants are the header's #defines."""
     src = open(HEADER).read()

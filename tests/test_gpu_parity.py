@@ -376,6 +376,50 @@ def test_batch_mixed_vs_oracle(gna, P, nbase, nbins, order):
     assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
+TOL_P_MIXED = 1e-6
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 1001, 100_003])
+def test_eval_mixed_vs_oracle(gna, n):
+    """NEXT-3 tier of the elementwise path (gna_oscprob_eval_ex, GNA_PREC_MIXED): 1e-6 absolute,
+    over the parity domain and the stress domain (angles up to pi/2, sum w <= 2)."""
+    g = synth.rng(950 + n)
+    for dom in (synth.PARITY_DOMAIN, dict(synth.PARITY_DOMAIN, theta12=(0, np.pi / 2),
+                                          theta13=(0, np.pi / 2))):
+        p = synth.random_params(g, domain=dom)
+        L = g.uniform(0, 300)
+        E = synth.random_energies(g, n)
+        P = _np(gna.oscprob_eval(p, L, _t(E), precision="mixed"))
+        Pr = oracle.prob_array(p, L, E, nthreads=_nt())
+        assert np.max(np.abs(P - Pr)) <= TOL_P_MIXED, (p, L)
+
+
+def test_eval_mixed_cfg3_full_size_sampled(gna):
+    """cfg3 through the TMA-fed stream in the mixed tier (FFMA2 pairs of energies)."""
+    import torch
+    c = synth.config("cfg3")
+    E = torch.linspace(c["lo"], c["hi"], c["n"], dtype=torch.float64, device="cuda")
+    P = gna.oscprob_eval(c["params"], c["L_km"], E, precision="mixed")
+    idx = np.r_[0:64, synth.rng(3).integers(0, c["n"], 10_000), c["n"] - 64:c["n"]]
+    it = torch.tensor(idx, device="cuda")
+    Es, Ps = _np(E[it]), _np(P[it])
+    assert np.max(np.abs(Ps - oracle.prob_array(c["params"], c["L_km"], Es))) <= TOL_P_MIXED
+    del E, P
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("nbins,order", [(1, 1), (37, 5), (1000, 10), (100_003, 10), (50, 32),
+                                         (64, 7)])
+def test_gl_integrate_mixed_vs_oracle(gna, nbins, order):
+    g = synth.rng(970 + nbins + order)
+    p = synth.random_params(g)
+    L = g.uniform(0, 300)
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    S = _np(gna.gl_integrate(p, L, _t(edges), order, precision="mixed"))
+    Sr = oracle.gl_integrate(p, L, edges, order, nthreads=_nt())
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_MIXED
+
+
 @pytest.mark.parametrize("cfg,idx", [("cfg5", [0, 417, 999]), ("cfg4", [0, 1, 5000, 9999])])
 def test_batch_mixed_full_size_sampled_and_split_invariant(gna, cfg, idx):
     """The mixed tier at the bench launch configuration (cfg5: per-point kernel; cfg4:

@@ -87,7 +87,7 @@ def main():
         with open(os.path.join(prof, "%s_bench_%s.jsonl" % (R, w)), "w") as f:
             f.write(json.dumps(d) + "\n")
         print("bench", w, "%.4g" % d["value"], d["unit"])
-    for w in ("cfg5", "cfg4"):
+    for w in ("cfg5", "cfg4", "cfg3", "cfg2"):
         p = os.path.join(src, "bench_%s_mixed.log" % w)
         if os.path.exists(p):
             d = last_json(p)

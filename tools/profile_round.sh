@@ -8,7 +8,7 @@ if [ -z "${PROF_ONLY:-}" ]; then
 for w in cfg5 cfg4 cfg3 cfg2 cfg1 cfg4grid cfg3emu cfg5fit; do
   timeout 400 python bench.py --workload $w > gpurun_out/final/bench_$w.log 2>&1; echo "$w rc=$?"
 done
-for w in cfg5 cfg4; do
+for w in cfg5 cfg4 cfg3 cfg2; do
   timeout 400 python bench.py --workload $w --precision mixed > gpurun_out/final/bench_${w}_mixed.log 2>&1
   echo "$w mixed rc=$?"
 done
