@@ -16,9 +16,7 @@
 #include <algorithm>
 #include <complex>
 #include <utility>
-#include <map>
 #include <mutex>
-#include <tuple>
 
 #include "../../include/gna_b200.h"
 #include "gna_common.cuh"
@@ -159,26 +157,6 @@ int sm_count() {
   return v;
 }
 
-// resident blocks per SM of a kernel at a dynamic smem size (occupancy API, cached per device)
-[[maybe_unused]] int resident_blocks(const void* kernel, int threads, size_t smem) {
-  static std::mutex mu;
-  static std::map<std::tuple<int, const void*, size_t>, int> cache;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
-  const auto key = std::make_tuple(dev, kernel, smem);
-  std::lock_guard<std::mutex> lk(mu);
-  const auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess ||
-      n < 1) {
-    cudaGetLastError();
-    n = 1;
-  }
-  cache.emplace(key, n);
-  return n;
-}
-
 // --- validation shared by device and host variants --------------------------
 int validate_eval(const gna_osc_params* p, double L_km, const double* E, int64_t n, const double* P) {
   if (!params_ok(p) || !E || !P || n < 1 || !is_fin(L_km) || L_km < 0) return GNA_EINVAL;
@@ -270,8 +248,7 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (e != cudaSuccess) return cuda_fail(e);
 
   const int nterm = 3 * nbase;
-  const size_t smem = (size_t)kBatchWarps * (GNA_SIN2_FQ ? nterm + (nterm + 3) / 4 : nterm) *
-                      sizeof(double2);
+  const size_t smem = (size_t)kBatchWarps * nterm * sizeof(double2);
   // node-group size: 5, 4 or 3 when it divides the order, else 4
   auto kern = (order % 5 == 0)   ? k_oscprob_batch<kBatchWarps, 5, kOut, kMixed>
               : (order % 4 == 0) ? k_oscprob_batch<kBatchWarps, 4, kOut, kMixed>
@@ -295,25 +272,6 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
             : (order % 4 == 0) ? k_oscprob_batch_pi<4, kOut, 3, kMixed>
             : (order % 3 == 0) ? k_oscprob_batch_pi<3, kOut, 3, kMixed>
                                : k_oscprob_batch_pi<4, kOut, 3, kMixed>;
-#endif
-#if GNA_BATCH_PI_TAIL
-    // Few waves (e.g. cfg4: ~8): pick the points per warp in [ppw/2, ppw] that minimises
-    // waves x (ppw + per-block overhead), so the last wave is not mostly idle
-    // (DESIGN.md §6.2).  The grouping never changes a point's result.
-    {
-      const int64_t hi = ppw;
-      double best = 0.0;
-      for (int64_t c = std::max<int64_t>(1, hi / 2); c <= hi; ++c) {
-        const size_t sm_c = (size_t)c * nterm * sizeof(double2) + (size_t)c * 33 * 8;
-        const int64_t slots = (int64_t)sm_count() * resident_blocks((const void*)kpi, 32, sm_c);
-        const int64_t nb = ((pts->npoints + c - 1) / c) * bpp;
-        const double cost = (double)((nb + slots - 1) / slots) * ((double)c + 0.25);
-        if (best == 0.0 || cost <= best) {
-          best = cost;
-          ppw = c;
-        }
-      }
-    }
 #endif
     const int64_t ng = (pts->npoints + ppw - 1) / ppw;
     const size_t smem_pi = (size_t)ppw * nterm * sizeof(double2) + (size_t)ppw * 33 * 8;

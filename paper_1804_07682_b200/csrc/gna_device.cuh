@@ -72,25 +72,6 @@ __device__ __forceinline__ double sin2c(double kq, double invE) {
   return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
 }
 
-// The same term with q = rint(y) found on the FP32 pipe (NEXT: one FP64 instruction fewer):
-// tf = kq_f * invE_f + 1.5*2^23 rounds in fp32; q is read from tf's bits with an integer
-// subtract and rebuilt as an exact double from the bits of 1.5*2^52 + 2^31 + q (one DADD).
-// q can differ from rint(y) by 1 only when y is within |y| * 2^-22 of a half-integer, so
-// |f| <= 0.5 + 2.5e-7 |y|; the minimax stays within 1.3e-16 for |f| <= 0.505, i.e. for
-// |y| <= 2e4.  Valid only for |y| < 2^22 (callers check the bound).
-constexpr double kRoundMagic31 = 6755401588539392.0;  // 1.5 * 2^52 + 2^31
-
-__device__ __forceinline__ double sin2c_fq(double kq, float kqf, double invE, float invEf) {
-  const float tf = fmaf(kqf, invEf, 12582912.0f);  // 1.5 * 2^23
-  const int qi = __float_as_int(tf) - 0x4B400000;
-  const double q = __hiloint2double(0x43380000, qi + (int)0x80000000) - kRoundMagic31;
-  const double f = fma(kq, invE, -q);
-  const double u = f * f;
-  const double p = sin2_poly(u);
-  const int odd = qi << 31;
-  return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
-}
-
 // Mixed tier.  The phase y = kq/E and its reduction stay
 // fp64 — they need it: y reaches ~1e3 and fp32 would lose the phase (ulp(550) = 6e-5).  The
 // reduction is taken modulo 2, y = 2m + 2h with m = rint(y/2), |h| <= 1/2 (three FP64
@@ -122,36 +103,11 @@ __device__ __forceinline__ f32x2 f2_mul(f32x2 a, f32x2 b) {
   return r;
 }
 
-#ifndef GNA_MIXED_CVT
-#define GNA_MIXED_CVT 0
-#endif
-
-// h = y/2 - rint(y/2) for y/2 = kqh * invE, rounded to fp32 by F2F (XU pipe, ~16 lanes/SM)
-__device__ __forceinline__ float mixed_h(double kqh, double invE) {
+// h = y/2 - rint(y/2) for y/2 = kqh * invE, rounded to fp32 (F2F, XU pipe)
+__device__ __forceinline__ float mixed_h1(double kqh, double invE) {
   const double t = fma(kqh, invE, kRoundMagic);
   const double m = t - kRoundMagic;
   return __double2float_rn(fma(kqh, invE, -m));
-}
-
-// The same h without a conversion instruction: the last FMA adds 1.5 * 2^29 - m instead of -m,
-// so the result C + h is rounded to the 2^-23 grid and its low word holds k = round(h 2^23)
-// (two's complement, |k| <= 2^22); C2 - t = 1.5*2^29 - m is exact.  The caller turns k into
-// fp32 with an integer add into 1.5*2^23's bit pattern and one (packed) FMA:
-// X = 1.5*2^23 + k exactly, h = X * 2^-23 - 1.5.  |h - h_fp64| <= 2^-24.
-constexpr double kRoundMagic29 = 6755400246362112.0;  // 1.5*2^52 + 1.5*2^29
-__device__ __forceinline__ int mixed_k(double kqh, double invE) {
-  const double t = fma(kqh, invE, kRoundMagic);
-  return __double2loint(fma(kqh, invE, kRoundMagic29 - t));
-}
-__device__ __forceinline__ float k_bits(int k) { return __int_as_float(0x4B400000 + k); }
-
-// fp32 h of one chain / of two chains packed, by the configured conversion
-__device__ __forceinline__ float mixed_h1(double kqh, double invE) {
-#if GNA_MIXED_CVT
-  return fmaf(k_bits(mixed_k(kqh, invE)), 0x1p-23f, -1.5f);
-#else
-  return mixed_h(kqh, invE);
-#endif
 }
 
 // W(h^2) = -cos(2 pi h)/2 for one chain
@@ -166,12 +122,7 @@ __device__ __forceinline__ float cos2_w(float h) {
 }
 
 __device__ __forceinline__ f32x2 mixed_h2(double kqa, double iEa, double kqb, double iEb) {
-#if GNA_MIXED_CVT
-  return f2_fma(f2_pack(k_bits(mixed_k(kqa, iEa)), k_bits(mixed_k(kqb, iEb))),
-                f2_pack(0x1p-23f, 0x1p-23f), f2_pack(-1.5f, -1.5f));
-#else
-  return f2_pack(mixed_h(kqa, iEa), mixed_h(kqb, iEb));
-#endif
+  return f2_pack(mixed_h1(kqa, iEa), mixed_h1(kqb, iEb));
 }
 
 // the same for two chains packed in one register pair

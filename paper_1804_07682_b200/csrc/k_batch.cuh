@@ -95,9 +95,6 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #ifndef GNA_BATCH_PI
 #define GNA_BATCH_PI 1
 #endif
-#ifndef GNA_SIN2_FQ
-#define GNA_SIN2_FQ 0
-#endif
 #ifndef GNA_BATCH_PI_Q2
 #define GNA_BATCH_PI_Q2 1
 #endif
@@ -109,9 +106,6 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #endif
 #ifndef GNA_BATCH_PPW_WORK
 #define GNA_BATCH_PPW_WORK 480
-#endif
-#ifndef GNA_BATCH_LDS_PREFETCH
-#define GNA_BATCH_LDS_PREFETCH 0
 #endif
 #ifndef GNA_BATCH_JUNROLL
 #define GNA_BATCH_JUNROLL 2
@@ -127,9 +121,6 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #endif
 #ifndef GNA_BATCH_PI_NT
 #define GNA_BATCH_PI_NT 1
-#endif
-#ifndef GNA_BATCH_PI_TAIL
-#define GNA_BATCH_PI_TAIL 0
 #endif
 #ifndef GNA_BATCH_PI_MINB
 #define GNA_BATCH_PI_MINB GNA_BATCH_MINB
@@ -177,37 +168,12 @@ __device__ __forceinline__ void batch_nodes(const double2* __restrict__ sc, int 
     }
     if constexpr (N & 1) a[N - 1] = (double)acc1;
   } else {
-#if GNA_SIN2_FQ
-  // q on the FP32 pipe: fp32 copies of the coefficients sit right after the double2 row
-  const float* __restrict__ scf = reinterpret_cast<const float*>(sc + nterm);
-  float iEf[N];
-#pragma unroll
-  for (int n = 0; n < N; ++n) iEf[n] = __double2float_rn(iE[n]);
-  for (int j = 0; j < nterm; ++j) {
-    const double2 cw = sc[j];
-    const float kf = scf[j];
-#pragma unroll
-    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c_fq(cw.x, kf, iE[n], iEf[n]), a[n]);
-  }
-#elif GNA_BATCH_LDS_PREFETCH
-  // the next coefficient pair is loaded before the current one is consumed, so the
-  // LDS latency is not exposed at the top of every iteration
-  double2 cw = sc[0];
-  GNA_UNROLL(GNA_BATCH_JUNROLL)
-  for (int j = 0; j < nterm; ++j) {
-    const double2 cn = sc[j + 1 < nterm ? j + 1 : j];
-#pragma unroll
-    for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
-    cw = cn;
-  }
-#else
   GNA_UNROLL(GNA_BATCH_JUNROLL)
   for (int j = 0; j < nterm; ++j) {
     const double2 cw = sc[j];
 #pragma unroll
     for (int n = 0; n < N; ++n) a[n] = fma(cw.y, gna::sin2c(cw.x, iE[n]), a[n]);
   }
-#endif
   }
 #pragma unroll
   for (int n = 0; n < N; ++n) {
@@ -273,7 +239,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const int64_t wt = (blockIdx.x - pg * bpp) * kWarps + warp;  // warp tile within a point
   const int64_t k0 = wt * 32;
   if (k0 >= nbins) return;  // whole warp
-  double2* sc = s_coef + warp * (GNA_SIN2_FQ ? nterm + (nterm + 3) / 4 : nterm);
+  double2* sc = s_coef + warp * nterm;
   const int64_t k = k0 + lane;
   const bool active = k < nbins;
   const int64_t kk = active ? k : nbins - 1;
@@ -289,9 +255,6 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
     __syncwarp();  // previous point's reads of sc are done
     for (int j = lane; j < nterm; j += 32) {
       sc[j] = stage_coef<kMixed>(gc[j]);
-#if GNA_SIN2_FQ
-      reinterpret_cast<float*>(sc + nterm)[j] = __double2float_rn(gc[j].x);
-#endif
     }
     __syncwarp();
     // bin = sum_n h w_n (c0 - a_n) = c0 W - A,  W = sum_n h w_n,  A = sum_n h w_n a_n

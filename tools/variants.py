@@ -13,12 +13,10 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "base": dict(),
-    "mx_magic": dict(GNA_MIXED_CVT=1),
     "mx_ju1": dict(GNA_MIXED_JUNROLL=1),
     "mx_n10": dict(GNA_MIXED_N10=1),
     "mx_n5": dict(GNA_MIXED_N10=0, GNA_MIXED_JUNROLL=2),
     "mx_n10_ju2": dict(GNA_MIXED_JUNROLL=2),
-    "mx_n10_magic": dict(GNA_MIXED_CVT=1),
     "mx_n10_ju1": dict(GNA_MIXED_N10=1, GNA_MIXED_JUNROLL=1),
     "mx_ju3": dict(GNA_MIXED_JUNROLL=3),
     "mx_ju4": dict(GNA_MIXED_JUNROLL=4),
@@ -32,15 +30,12 @@ VARIANTS = {
     "d7_ju8": dict(GNA_BATCH_JUNROLL=8),
     "d7_ju2_mb20": dict(GNA_BATCH_JUNROLL=2, GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
     "d7_pim20": dict(GNA_BATCH_PI_MINB=20),
-    "d7_lds": dict(GNA_BATCH_LDS_PREFETCH=1),
     "pi_m20": dict(GNA_BATCH_PI_MINB=20),
     "pi_m18": dict(GNA_BATCH_PI_MINB=18),
     "pi_m24": dict(GNA_BATCH_PI_MINB=24),
     "pi_nt3": dict(GNA_BATCH_PI_NT=1),
-    "deg7": dict(GNA_SIN2_DEG=7),
+    "deg8": dict(GNA_SIN2_DEG=8),
     "mb20": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1),
-    "notail": dict(GNA_BATCH_PI_TAIL=0),
-    "tail_m20": dict(GNA_BATCH_PI_MINB=20),
     "mb20_nt3": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1, GNA_BATCH_PI_NT=1),
     "pi_nt3_m16": dict(GNA_BATCH_PI_NT=1, GNA_BATCH_PI_MINB=16),
     "pi_m20_w240": dict(GNA_BATCH_PI_MINB=20, GNA_BATCH_PPW_WORK=240),
