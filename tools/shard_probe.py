@@ -13,7 +13,8 @@ import paper_1804_07682_b200 as gna  # noqa: E402
 import synth  # noqa: E402
 
 
-def main():
+def main(precision="fp64"):
+    print("# precision:", precision)
     dev = torch.device("cuda", 0)
     c = synth.config("cfg5")
     f64 = dict(dtype=torch.float64, device=dev)
@@ -29,7 +30,7 @@ def main():
         x2 = torch.empty(P, **f64)
         ws = torch.empty(gna.oscprob_batch_workspace_size(P, 8, nb, 10) // 8 + 2, **f64)
         call = lambda: gna.oscprob_batch(pts, c["L_km"], c["omega"], edges, 10, data=data,  # noqa
-                                         spectra=sp, chi2=x2, workspace=ws)
+                                         spectra=sp, chi2=x2, workspace=ws, precision=precision)
         call()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
@@ -56,4 +57,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(*sys.argv[1:])
