@@ -206,6 +206,25 @@ int64_t blocks_per_point(int64_t nbins) {
   return (warps_per_point(nbins) + kBatchWarps - 1) / kBatchWarps;
 }
 
+// <<<grid, block, smem, s>>> with the programmatic-stream-serialization attribute (PDL): the
+// kernel may start while its predecessor on the stream finishes; it synchronises in-kernel
+// (pdl_wait) before touching the predecessor's outputs.
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = GNA_PDL ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // launch of the batch kernels on already-validated device arguments
 template <int kOut, bool kMixed>
 int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double* omega,
@@ -275,11 +294,13 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
 #endif
     const int64_t ng = (pts->npoints + ppw - 1) / ppw;
     const size_t smem_pi = (size_t)ppw * nterm * sizeof(double2) + (size_t)ppw * 33 * 8;
-    kpi<<<(unsigned)(ng * bpp), 32, smem_pi, s>>>(nterm, order, nbins, pts->npoints, bpp,
-                                                  (int)ppw, w, spectra, chi2 ? data : nullptr);
+    e = launch_pdl(kpi, (unsigned)(ng * bpp), 32, smem_pi, s, nterm, order, nbins, pts->npoints,
+                   bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e);
   } else {
-    kern<<<(unsigned)nblocks, kBatchWarps * 32, smem, s>>>(
-        nterm, order, nbins, pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
+    e = launch_pdl(kern, (unsigned)nblocks, kBatchWarps * 32, smem, s, nterm, order, nbins,
+                   pts->npoints, bpp, (int)ppw, w, spectra, chi2 ? data : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
@@ -287,8 +308,9 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (chi2) {
     const int64_t threads = pts->npoints * 32;
     const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
-    k_chi2_reduce<kOut><<<grid, kReduceThreads, 0, s>>>(w.partial, pts->npoints,
-                                                        warps_per_point(nbins), chi2);
+    e = launch_pdl(k_chi2_reduce<kOut>, (unsigned)grid, kReduceThreads, 0, s,
+                   (const double*)w.partial, pts->npoints, warps_per_point(nbins), chi2);
+    if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);

@@ -15,6 +15,23 @@ struct BatchSetupArgs {
   int64_t npoints;
 };
 
+// Programmatic dependent launch (sm_90+; GNA_PDL): the main pass is launched while the setup
+// kernel still runs and waits for it here; the chi2 reduce likewise waits for the main pass.
+// Without a programmatic dependency both instructions are no-ops.
+#ifndef GNA_PDL
+#define GNA_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if GNA_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if GNA_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // Workspace layout of the batch path (all offsets 16-byte aligned), see
 // gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
 // c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp].
@@ -59,6 +76,7 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
                                                      const double* __restrict__ d21,
                                                      const double* __restrict__ d31,
                                                      const double* __restrict__ edges, BatchWs w) {
+  pdl_launch_dependents();  // the main pass may be scheduled now; it waits in pdl_wait()
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = a.npoints * a.nbase;
   const int64_t n2 = (int64_t)a.order * a.nbins;
@@ -248,6 +266,7 @@ __global__ void __launch_bounds__(kWarps * 32, GNA_BATCH_MINB) k_oscprob_batch(
   const double D = (data && active) ? data[k] : 1.0;
   const double iD = 1.0 / D;  // once per lane: chi2 terms d^2 / D as d^2 * iD (no per-point divide)
   const int64_t wpp = warps_per_point_dev(nbins);
+  pdl_wait();  // the setup kernel's tables are complete and visible
   // ppw points per warp, same bins: the node tables stay in L1 across points
   const int64_t pend = min(npoints, (pg + 1) * (int64_t)ppw);
   for (int64_t p = pg * (int64_t)ppw; p < pend; ++p) {
@@ -302,6 +321,7 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
   if (k0 >= nbins) return;
   const int64_t p0 = pg * (int64_t)ppw;
   const int np = (int)min((int64_t)ppw, npoints - p0);
+  pdl_wait();  // the setup kernel's tables are complete and visible
   for (int j = lane; j < np * nterm; j += 32) sc[j] = stage_coef<kMixed>(w.coef[p0 * nterm + j]);
   for (int j = lane; j < np; j += 32) s_c0[j] = w.c0[p0 + j];
   for (int q = 0; q < np; ++q) s_acc[q * 32 + lane] = 0.0;
@@ -437,6 +457,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __
                                                                 double* __restrict__ chi2) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_wait();  // every partial of the main pass is written
   if (p >= npoints) return;
   const double* q = partial + p * wpp;
   double s = 0.0;

@@ -13,6 +13,7 @@ from paper_1804_07682_b200 import _build  # noqa: E402
 
 VARIANTS = {
     "base": dict(),
+    "nopdl": dict(GNA_PDL=0),
     "mx_ju1": dict(GNA_MIXED_JUNROLL=1),
     "mx_n10": dict(GNA_MIXED_N10=1),
     "mx_n5": dict(GNA_MIXED_N10=0, GNA_MIXED_JUNROLL=2),
