@@ -126,6 +126,8 @@ int gna_oscprob_eval_ab(int32_t alpha, int32_t beta, const gna_osc_params* p, do
  * d_edges: device [nbins + 1] bin edges in MeV (strictly increasing, > 0).
  * order in [1, GNA_MAX_ORDER].  d_bins: device [nbins] output.
  * EINVAL as for gna_oscprob_eval, plus nbins < 1 or order out of range.
+ * A bin's value depends only on its two edges (bitwise: the same for any nbins and
+ * any split of the edges between calls).
  * ------------------------------------------------------------------------- */
 int gna_gl_integrate(const gna_osc_params* p, double L_km, const double* d_edges, int64_t nbins,
                      int32_t order, double* d_bins, void* stream);

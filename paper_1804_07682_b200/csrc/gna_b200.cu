@@ -277,7 +277,31 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   // mixed tier: 10 nodes (5 packed pairs) per coefficient load when the order allows
   if (kMixed && order % 10 == 0) kern = k_oscprob_batch<kBatchWarps, 10, kOut, kMixed>;
 #endif
-  if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
+  int pt_sub = 1;  // chi2 sub-partials per tile (k_oscprob_batch_pt)
+  if (!kMixed && GNA_BATCH_PT && kBatchWarps == 1 && (nterm == 3 || nterm == 6) &&
+      pts->npoints >= GNA_BATCH_PT_MIN_POINTS) {
+    // many points, few terms: points across lanes, 32-bin tiles (bitwise-identical sums)
+    auto kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 3, kOut>
+               : (order % 4 == 0) ? k_oscprob_batch_pt<4, 3, kOut>
+               : (order % 3 == 0) ? k_oscprob_batch_pt<3, 3, kOut>
+                                  : k_oscprob_batch_pt<4, 3, kOut>;
+    if (nterm == 6)
+      kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 6, kOut>
+            : (order % 4 == 0) ? k_oscprob_batch_pt<4, 6, kOut>
+            : (order % 3 == 0) ? k_oscprob_batch_pt<3, 6, kOut>
+                               : k_oscprob_batch_pt<4, 6, kOut>;
+#if GNA_BATCH_PT_N10
+    if (order % 10 == 0) kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut> : k_oscprob_batch_pt<10, 6, kOut>;
+#endif
+    const int64_t ng = (pts->npoints + 31) / 32;
+    const size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);
+    pt_sub = GNA_BATCH_PT_SUB;
+    const int lv = pt_sub == 4 ? 3 : pt_sub == 2 ? 4 : 5;
+    if (ng * bpp * pt_sub > 0x7fffffffLL) return GNA_EINVAL;
+    e = launch_pdl(kpt, (unsigned)(ng * bpp * pt_sub), 32, smem_pt, s, (int)order, nbins,
+                   pts->npoints, bpp, lv, w, spectra, chi2 ? data : nullptr);
+    if (e != cudaSuccess) return cuda_fail(e);
+  } else if (ppw > 1 && small_terms && kBatchWarps == 1 && GNA_BATCH_PI) {
     // several points per warp: node groups outer, points inner (bitwise-identical sums)
     ppw = std::min<int64_t>(ppw, kMaxPPW);
     auto kpi = (order % 5 == 0)   ? k_oscprob_batch_pi<5, kOut, 0, kMixed>
@@ -308,7 +332,9 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (chi2) {
     const int64_t threads = pts->npoints * 32;
     const int grid = (int)((threads + kReduceThreads - 1) / kReduceThreads);
-    e = launch_pdl(k_chi2_reduce<kOut>, (unsigned)grid, kReduceThreads, 0, s,
+    auto kred = pt_sub == 4 ? k_chi2_reduce<kOut, 4>
+                : pt_sub == 2 ? k_chi2_reduce<kOut, 2> : k_chi2_reduce<kOut, 1>;
+    e = launch_pdl(kred, (unsigned)grid, kReduceThreads, 0, s,
                    (const double*)w.partial, pts->npoints, warps_per_point(nbins), chi2);
     if (e != cudaSuccess) return cuda_fail(e);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -372,11 +398,20 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
 template <class Coef>
 int launch_gl(const Coef& c, const double* edges, int64_t nbins, int order, double* bins,
               cudaStream_t s) {
-  const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
-  if (grid > 0x7fffffffLL) return GNA_EINVAL;
-  const gl_kernel_t<Coef> kern =
-      gl_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
-  kern<<<(unsigned)grid, kGLLaneThreads, 0, s>>>(c, edges, nbins, bins);
+  if (nbins >= (int64_t)GNA_GL_TB_MIN_BINS) {
+    // thread per bin, GL table as uniform constant-bank operands (k_gl.cuh)
+    const int64_t grid = (nbins + kGLTbThreads - 1) / kGLTbThreads;
+    if (grid > 0x7fffffffLL) return GNA_EINVAL;
+    const gl_kernel_t<Coef> kern =
+        gl_tb_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+    kern<<<(unsigned)grid, kGLTbThreads, 0, s>>>(c, edges, nbins, bins);
+  } else {
+    const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
+    if (grid > 0x7fffffffLL) return GNA_EINVAL;
+    const gl_kernel_t<Coef> kern =
+        gl_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+    kern<<<(unsigned)grid, kGLLaneThreads, 0, s>>>(c, edges, nbins, bins);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);

@@ -34,7 +34,8 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 
 // Workspace layout of the batch path (all offsets 16-byte aligned), see
 // gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
-// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp].
+// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp][S] (S = 1 except for
+// k_oscprob_batch_pt sub-tiles; sized for S = kPtSubMax).
 struct BatchWs {
   double2* coef;
   double* c0;
@@ -45,11 +46,15 @@ struct BatchWs {
 
 
 
+// chi2 partials per (point, 32-bin tile); the points-across-lanes kernel may split a tile
+// into up to kPtSubMax sub-tiles, each with its own partial (k_oscprob_batch_pt)
+constexpr int kPtSubMax = 4;
+
 size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
   size_t b = align16((size_t)P * nbase * 3 * sizeof(double2));
   b += align16((size_t)P * sizeof(double));
   b += 2 * align16((size_t)order * nbins * sizeof(double));
-  if (chi2) b += align16((size_t)P * warps_per_point(nbins) * sizeof(double));
+  if (chi2) b += align16((size_t)P * warps_per_point(nbins) * kPtSubMax * sizeof(double));
   return b;
 }
 
@@ -449,9 +454,165 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
   if constexpr (kOut != kOutLocal) __threadfence_system();
 }
 
+// Points-across-lanes variant (few terms, many points: cfg4's single-baseline scan).  Block
+// = one warp = 32 consecutive points x one 32-bin tile.  Each lane keeps its point's NT
+// coefficients in registers; the tile's node tables (1/E, h w), W, D and 1/D are staged once
+// into shared memory and read back as warp-uniform broadcasts, bin by bin.  Compared with
+// k_oscprob_batch_pi this drops the per-bin chi2 shuffle tree and the idle lanes of the
+// ragged last bin tile (nbins = 1000 = 31.25 tiles), and the per-point shared-memory
+// accumulators.  Results are bitwise identical to k_oscprob_batch: the same operations in
+// the same order per (point, bin), and the tile's chi2 partial is the same xor-tree sum —
+// the bins are visited in bit-reversed order, which turns the tree into consecutive pairs,
+// summed online with a 5-level binary counter.
+#ifndef GNA_BATCH_PT
+#define GNA_BATCH_PT 1
+#endif
+#ifndef GNA_BATCH_PT_MINB
+#define GNA_BATCH_PT_MINB 1
+#endif
+#ifndef GNA_BATCH_PT_SUB
+#define GNA_BATCH_PT_SUB 2  // sub-tiles per 32-bin tile: 1, 2 or 4
+#endif
+#ifndef GNA_BATCH_PT_MUNROLL
+#define GNA_BATCH_PT_MUNROLL 1
+#endif
+#ifndef GNA_BATCH_PT_N10
+#define GNA_BATCH_PT_N10 0
+#endif
+#ifndef GNA_BATCH_PT_MIN_POINTS
+#define GNA_BATCH_PT_MIN_POINTS 256
+#endif
+
+template <int N, int NT>
+__device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&cw)[NT],
+                                         const double* __restrict__ sE,
+                                         const double* __restrict__ sH, int b, int i, double& A) {
+  double iE[N], a[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    iE[n] = sE[(i + n) * 32 + b];
+    a[n] = 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) a[n] = fma(cw[j], gna::sin2c(kq[j], iE[n]), a[n]);
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) A = fma(sH[(i + n) * 32 + b], a[n], A);
+}
+
+template <int N, int NT>
+__device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const double (&cw)[NT],
+                                        const double* __restrict__ sE,
+                                        const double* __restrict__ sH, int b, int i, double& A) {
+  if constexpr (N > 1) {
+    if (r == N - 1) {
+      pt_nodes<N - 1, NT>(kq, cw, sE, sH, b, i, A);
+      return;
+    }
+    pt_tail<N - 1, NT>(r, kq, cw, sE, sH, b, i, A);
+  }
+}
+
+// A tile may be split into S = 2^(5 - lv) sub-tiles of 2^lv consecutive visits (more,
+// shorter warps: a smaller last wave); each sub-tile's tree sum is a chi2 sub-partial and
+// k_chi2_reduce<S> finishes the tree's top levels.
+template <int N, int NT, int kOut>
+__global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
+    int order, int64_t nbins, int64_t npoints, int64_t bpp, int lv, BatchWs w,
+    double* __restrict__ spectra, const double* __restrict__ data) {
+  extern __shared__ double s_pt[];
+  double* sE = s_pt;                // [order][32] 1/E of the tile's nodes
+  double* sH = sE + order * 32;     // [order][32] h w
+  double* sW = sH + order * 32;     // [32] sum_i h w_i (same order as k_oscprob_batch)
+  double* sD = sW + 32;             // [32] data
+  double* sID = sD + 32;            // [32] 1 / data
+  const int lane = threadIdx.x & 31;
+  const int S = 32 >> lv;
+  const int64_t tile = blockIdx.x / S;  // (point group, bin tile)
+  const int sub = (int)(blockIdx.x - tile * S);
+  const int64_t pg = tile / bpp;
+  const int64_t wt = tile - pg * bpp;
+  const int64_t k0 = wt * 32;
+  const int64_t p = pg * 32 + lane;
+  const bool pact = p < npoints;
+  const int64_t pp = pact ? p : npoints - 1;
+  {
+    const int64_t k = k0 + lane;
+    const bool kact = k < nbins;
+    const int64_t kk = kact ? k : nbins - 1;
+    const double D = (data && kact) ? data[k] : 1.0;
+    sD[lane] = D;
+    sID[lane] = 1.0 / D;
+    pdl_wait();  // the setup kernel's tables are complete and visible
+    double W = 0.0;
+    for (int i = 0; i < order; ++i) {
+      const double h = w.hw[(int64_t)i * nbins + kk];
+      sE[i * 32 + lane] = w.invE[(int64_t)i * nbins + kk];
+      sH[i * 32 + lane] = h;
+      W += h;
+    }
+    sW[lane] = W;
+  }
+  double kq[NT], cw[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
+    const double2 c = w.coef[pp * NT + j];
+    kq[j] = c.x;
+    cw[j] = c.y;
+  }
+  const double c0 = w.c0[pp];
+  __syncwarp();
+  // chi2 partial of the tile = xor tree over its 32 bins (k_oscprob_batch); visited in
+  // bit-reversed order the tree pairs consecutive visits: r[l] holds the pending left
+  // operand of level l, and after the sub-tile's last visit x2 is its subtree sum
+  double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double x2 = 0.0;
+  double* __restrict__ out = spectra ? spectra + pp * nbins : nullptr;
+  const int m0 = sub << lv;
+  GNA_UNROLL(GNA_BATCH_PT_MUNROLL)
+  for (int m = m0; m < m0 + (1 << lv); ++m) {
+    const int b = (int)(__brev((unsigned)m) >> 27);
+    double A = 0.0;
+    int i = 0;
+    for (; i + N <= order; i += N) pt_nodes<N, NT>(kq, cw, sE, sH, b, i, A);
+    if (i < order) pt_tail<N, NT>(order - i, kq, cw, sE, sH, b, i, A);
+    const double s = fma(c0, sW[b], -A);
+    x2 = 0.0;
+    // bins past the end of a ragged tile are computed and dropped: skipping them with a
+    // warp-uniform branch measured 1 % slower on cfg4 (357.5 vs 361.7 G/s)
+    if (k0 + b < nbins) {
+      if (out && pact) out_store<kOut>(out + k0 + b, s);
+      const double d = s - sD[b];
+      x2 = d * d * sID[b];
+    }
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      if (l >= lv) break;
+      if (!(m & (1 << l))) {
+        r[l] = x2;
+        break;
+      }
+      x2 = r[l] + x2;
+    }
+  }
+  if (w.partial && pact) w.partial[(p * warps_per_point_dev(nbins) + wt) * S + sub] = x2;
+  if constexpr (kOut != kOutLocal) __threadfence_system();
+}
+
 // chi2[p] = sum of the point's warp partials: lane l folds partials l, l+32, ...
 // in order, then a fixed xor tree (deterministic, independent of scheduling).
-template <int kOut>
+// With S > 1 (k_oscprob_batch_pt sub-tiles) a tile's partial is first assembled from its S
+// sub-partials by the top levels of the same tree.
+template <int S>
+__device__ __forceinline__ double tile_partial(const double* __restrict__ q, int64_t j) {
+  if constexpr (S == 1) return q[j];
+  else if constexpr (S == 2) return q[2 * j] + q[2 * j + 1];
+  else return (q[4 * j] + q[4 * j + 1]) + (q[4 * j + 2] + q[4 * j + 3]);
+}
+
+template <int kOut, int S = 1>
 __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __restrict__ partial,
                                                                 int64_t npoints, int64_t wpp,
                                                                 double* __restrict__ chi2) {
@@ -459,9 +620,9 @@ __global__ void __launch_bounds__(kReduceThreads) k_chi2_reduce(const double* __
   const int lane = threadIdx.x & 31;
   pdl_wait();  // every partial of the main pass is written
   if (p >= npoints) return;
-  const double* q = partial + p * wpp;
+  const double* q = partial + p * wpp * S;
   double s = 0.0;
-  for (int64_t j = lane; j < wpp; j += 32) s += q[j];
+  for (int64_t j = lane; j < wpp; j += 32) s += tile_partial<S>(q, j);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out_store<kOut>(chi2 + p, s);

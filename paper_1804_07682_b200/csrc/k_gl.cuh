@@ -40,16 +40,68 @@ __global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Co
     iE[i] = gna::rcp(fma(h, __ldg(&g_gl_t[off + node]), ctr));
   }
   gna::prob_inv_n<H>(c, iE, pv);
+  // s_half = sum over the lane's nodes, ascending, of w_i P_i (explicit FMAs: the same
+  // arithmetic as k_gl_integrate_tb, so a bin's value does not depend on nbins)
+  double s = 0.0;
 #pragma unroll
   for (int i = 0; i < H; ++i) {
     const int node = half * H + i;
-    pv[i] = node < kOrder ? __ldg(&g_gl_w[off + node]) * pv[i] : 0.0;
+    if (node < kOrder) s = fma(__ldg(&g_gl_w[off + node]), pv[i], s);
   }
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < H; ++i) s += pv[i];
   const double other = __shfl_xor_sync(0xffffffffu, s, 1);
   if (act && half == 0) bins[k] = h * (s + other);
+}
+
+// Large nbins: one thread per bin.  All lanes of a warp visit the same node index at the
+// same time, so the GL nodes and weights come from the constant bank as uniform operands
+// (no table loads); the nodes are taken G at a time (G divides the order when it can),
+// each group's reciprocals and three sin^2 terms forming G independent chains.  The
+// weighted node sum is formed exactly as in the lane-pair kernel (two ascending halves,
+// then h (s0 + s1)), so both kernels give the same bits for a bin.  Measured against the
+// lane-pair kernel (tools/gl_sweep.py, profiles/r01_gl_sweep.jsonl): equal up to 10^5 bins
+// (both at the launch floor), 1.12x (GL10) / 1.38x (GL5) at 10^6 bins, 1.13x / 1.41x at 10^7.
+#ifndef GNA_GL_TB_MINB
+#define GNA_GL_TB_MINB 4
+#endif
+#ifndef GNA_GL_TB_MIN_BINS
+#define GNA_GL_TB_MIN_BINS 32768  // below: lane pairs (latency); above: thread per bin
+#endif
+constexpr int kGLTbThreads = 128;
+
+__host__ __device__ constexpr int gl_group(int order) {
+  return order % 5 == 0 ? 5 : order % 4 == 0 ? 4 : order % 3 == 0 ? 3 : order < 5 ? order : 5;
+}
+
+template <int kOrder, class Coef>
+__global__ void __launch_bounds__(kGLTbThreads, GNA_GL_TB_MINB) k_gl_integrate_tb(
+    Coef c, const double* __restrict__ edges, int64_t nbins, double* __restrict__ bins) {
+  constexpr int G = gl_group(kOrder);
+  constexpr int off = GNA_GL_OFF(kOrder);
+  const int64_t k = (int64_t)blockIdx.x * kGLTbThreads + threadIdx.x;
+  if (k >= nbins) return;
+  const double e0 = edges[k], e1 = edges[k + 1];
+  const double ctr = 0.5 * (e0 + e1);
+  const double h = 0.5 * (e1 - e0);
+  constexpr int H = (kOrder + 1) / 2;
+  double s0 = 0.0, s1 = 0.0;  // nodes [0, H) and [H, order): the lane-pair kernel's halves
+#pragma unroll
+  for (int i0 = 0; i0 < kOrder; i0 += G) {
+    const int n = kOrder - i0 < G ? kOrder - i0 : G;
+    double iE[G], pv[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) iE[i] = gna::rcp(fma(h, c_gl_t[off + (i < n ? i0 + i : i0)], ctr));
+    gna::prob_inv_n<G>(c, iE, pv);
+#pragma unroll
+    for (int i = 0; i < G; ++i) {
+      if (i < n) {
+        if (i0 + i < H)
+          s0 = fma(c_gl_w[off + i0 + i], pv[i], s0);
+        else
+          s1 = fma(c_gl_w[off + i0 + i], pv[i], s1);
+      }
+    }
+  }
+  bins[k] = h * (s0 + s1);
 }
 
 template <class Coef>
@@ -58,6 +110,12 @@ using gl_kernel_t = void (*)(Coef, const double*, int64_t, double*);
 template <class Coef, int... N>
 gl_kernel_t<Coef> gl_kernel_for(int order, std::integer_sequence<int, N...>) {
   static const gl_kernel_t<Coef> t[] = {k_gl_integrate<N + 1, Coef>...};
+  return t[order - 1];
+}
+
+template <class Coef, int... N>
+gl_kernel_t<Coef> gl_tb_kernel_for(int order, std::integer_sequence<int, N...>) {
+  static const gl_kernel_t<Coef> t[] = {k_gl_integrate_tb<N + 1, Coef>...};
   return t[order - 1];
 }
 

@@ -290,6 +290,20 @@ def test_gl_ragged_sizes(gna, nbins):
     assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
 
 
+@pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 7, 10, 11, 13, 16, 29, 32])
+def test_gl_thread_per_bin_path_all_group_shapes(gna, order):
+    # nbins above GNA_GL_TB_MIN_BINS (32768): the thread-per-bin kernel, node groups of
+    # 5/4/3 and the ragged last group (orders 7, 11, 13, 29)
+    g = synth.rng(1300 + order)
+    p = synth.random_params(g)
+    L = g.uniform(1, 300)
+    nbins = 40_001
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    S = _np(gna.gl_integrate(p, L, _t(edges), order))
+    Sr = oracle.gl_integrate(p, L, edges, order, nthreads=_nt())
+    assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
+
+
 def test_gl_zero_mixing_is_bin_width(gna):
     e = synth.uniform_edges(333, 1.0, 10.0)
     p0 = dict(synth.CANONICAL, theta12=0.0, theta13=0.0)
@@ -440,6 +454,30 @@ def test_batch_mixed_full_size_sampled_and_split_invariant(gna, cfg, idx):
         sps, x2s = _run_batch(gna, s2, c["L_km"], c["omega"], c["edges"], c["order"], c["data"],
                               precision="mixed")
         assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi])
+
+
+@pytest.mark.parametrize("nbase,nbins,order", [(1, 1000, 10), (1, 257, 7), (2, 300, 5),
+                                               (1, 33, 32), (2, 1, 1)])
+def test_batch_points_across_lanes_path_vs_oracle_and_bitwise(gna, nbase, nbins, order):
+    """>= 256 points and <= 2 baselines: the points-across-lanes kernel.  Sampled parity with
+    the oracle, and bitwise equality with the other batch kernels (a 100-point call runs the
+    points-inner or per-point kernel), incl. chi2 (same xor-tree order)."""
+    g = synth.rng(1500 + nbase * nbins + order)
+    pts, L, om, edges, data = _batch_case(g, 611, nbase, nbins, order)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data)
+    idx = np.array([0, 31, 32, 300, 607, 610])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, data))
+    for lo, hi in ((0, 100), (100, 611), (1, 2)):
+        s2 = synth.subset_points(pts, np.arange(lo, hi))
+        sps, x2s = _run_batch(gna, s2, L, om, edges, order, data)
+        assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi]), (lo, hi)
+    # chi2-only / spectra-only give the same bits
+    sp2, _ = _run_batch(gna, pts, L, om, edges, order, None)
+    _, x22 = _run_batch(gna, pts, L, om, edges, order, data, spectra=False)
+    assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
 def test_batch_single_baseline_matches_gl_integrate(gna):
