@@ -66,7 +66,10 @@ __global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Co
 #ifndef GNA_GL_TB_MIN_BINS
 #define GNA_GL_TB_MIN_BINS 32768  // below: lane pairs (latency); above: thread per bin
 #endif
-constexpr int kGLTbThreads = 128;
+#ifndef GNA_GL_TB_THREADS
+#define GNA_GL_TB_THREADS 128
+#endif
+constexpr int kGLTbThreads = GNA_GL_TB_THREADS;
 
 __host__ __device__ constexpr int gl_group(int order) {
   return order % 5 == 0 ? 5 : order % 4 == 0 ? 4 : order % 3 == 0 ? 3 : order < 5 ? order : 5;

@@ -32,7 +32,8 @@ WORKLOADS = ["cfg5", "cfg4", "cfg3", "cfg2", "cfg1", "cfg4grid", "cfg3emu", "cfg
 # capture name -> (workload it was captured on, kernel label for ncu_traffic.json)
 CAPTURES = {
     "batch": ("cfg5", "k_oscprob_batch"),
-    "batch_pi": ("cfg4", "k_oscprob_batch_pi"),
+    "batch_pt": ("cfg4", "k_oscprob_batch_pt"),
+    "batch_pi_mixed": ("cfg4_mixed", "k_oscprob_batch_pi<..., kMixed>"),
     "eval": ("cfg3", "k_oscprob_eval_tma"),
     "eval_ab": ("cfg3emu", "k_oscprob_eval_tma<PabCoef>"),
     "gl": ("cfg2", "k_gl_integrate"),
