@@ -247,13 +247,16 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   const BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
   const int64_t bpp = blocks_per_point(nbins);
   // points per warp: enough sin^2 work per lane to amortise the per-point overhead
-  // (>= 240; >= GNA_BATCH_PPW_WORK for the small-nbase points-inner kernel), while
-  // keeping >= 16 warps per SM worth of blocks
+  // (>= GNA_BATCH_PPW_WORK_BIG; >= GNA_BATCH_PPW_WORK for the small-nbase points-inner
+  // kernel), while keeping >= 16 warps per SM worth of blocks — for the per-point kernel
+  // >= GNA_BATCH_PPW_MIN_WAVES such waves, so the longer warps do not leave a costly last
+  // wave (cfg5: ppw 2, +0.5 %; the 81-point fit step stays at ppw 1, where ppw 2 lost 2 %)
   const int64_t work = (int64_t)3 * nbase * order;
   const bool small_terms = 3 * nbase <= GNA_BATCH_PI_MAX_TERMS;
   int64_t ppw = std::max<int64_t>(
       1, ((small_terms ? GNA_BATCH_PPW_WORK : GNA_BATCH_PPW_WORK_BIG) + work - 1) / work);
-  const int64_t min_blocks = (int64_t)sm_count() * 16;
+  const int64_t min_blocks =
+      (int64_t)sm_count() * 16 * (small_terms ? 1 : GNA_BATCH_PPW_MIN_WAVES);
   while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
   const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;
   const int64_t nblocks = ngroups * bpp;

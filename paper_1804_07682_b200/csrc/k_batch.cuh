@@ -125,7 +125,10 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
 #define GNA_BATCH_PI_MAX_TERMS 6
 #endif
 #ifndef GNA_BATCH_PPW_WORK_BIG
-#define GNA_BATCH_PPW_WORK_BIG 240
+#define GNA_BATCH_PPW_WORK_BIG 480
+#endif
+#ifndef GNA_BATCH_PPW_MIN_WAVES
+#define GNA_BATCH_PPW_MIN_WAVES 32
 #endif
 #ifndef GNA_BATCH_PPW_WORK
 #define GNA_BATCH_PPW_WORK 480
