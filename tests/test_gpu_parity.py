@@ -718,10 +718,11 @@ def test_repeated_calls_bitwise_deterministic(gna):
 
 
 # ------------------------------------------------------------------------ NEXT-4 fused gather
-def test_fused_gather_epilogue_single_rank(gna):
+@pytest.mark.parametrize("P,nbase", [(13, 3), (300, 1)])
+def test_fused_gather_epilogue_single_rank(gna, P, nbase):
     """gna_oscprob_batch_ex writing through symmetric memory (1-rank group on this one
     GPU): peer-window stores and, where the fabric allows it, multicast stores give the
-    same bits as the plain batch."""
+    same bits as the plain batch (per-point kernel; points-across-lanes kernel at 300x1)."""
     import socket
 
     import torch
@@ -729,7 +730,7 @@ def test_fused_gather_epilogue_single_rank(gna):
 
     from paper_1804_07682_b200 import dist as gdist
     g = synth.rng(81)
-    pts, L, om, edges, data = _batch_case(g, 13, 3, 200, 10)
+    pts, L, om, edges, data = _batch_case(g, P, nbase, 200, 10)
     dp = {k: _t(v) for k, v in pts.items()}
     de, dd = _t(edges), _t(data)
     ref_sp, ref_x2 = gna.oscprob_batch(dp, L, om, de, 10, data=dd)
@@ -744,7 +745,7 @@ def test_fused_gather_epilogue_single_rank(gna):
         modes = [False, True]
         seen = []
         for prefer_mc in modes:
-            fg = gdist.FusedGather(13, 200, "cuda", prefer_multicast=prefer_mc)
+            fg = gdist.FusedGather(P, 200, "cuda", prefer_multicast=prefer_mc)
             if prefer_mc and not fg.multicast:
                 continue
             fg.spectra.fill_(float("nan"))
