@@ -281,20 +281,25 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   if (kMixed && order % 10 == 0) kern = k_oscprob_batch<kBatchWarps, 10, kOut, kMixed>;
 #endif
   int pt_sub = 1;  // chi2 sub-partials per tile (k_oscprob_batch_pt)
-  if (!kMixed && GNA_BATCH_PT && kBatchWarps == 1 && (nterm == 3 || nterm == 6) &&
-      pts->npoints >= GNA_BATCH_PT_MIN_POINTS) {
+  if ((GNA_BATCH_PT_MIXED || !kMixed) && GNA_BATCH_PT && kBatchWarps == 1 &&
+      (nterm == 3 || nterm == 6) && pts->npoints >= GNA_BATCH_PT_MIN_POINTS) {
     // many points, few terms: points across lanes, 32-bin tiles (bitwise-identical sums)
-    auto kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 3, kOut>
-               : (order % 4 == 0) ? k_oscprob_batch_pt<4, 3, kOut>
-               : (order % 3 == 0) ? k_oscprob_batch_pt<3, 3, kOut>
-                                  : k_oscprob_batch_pt<4, 3, kOut>;
+    auto kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 3, kOut, kMixed>
+               : (order % 4 == 0) ? k_oscprob_batch_pt<4, 3, kOut, kMixed>
+               : (order % 3 == 0) ? k_oscprob_batch_pt<3, 3, kOut, kMixed>
+                                  : k_oscprob_batch_pt<4, 3, kOut, kMixed>;
     if (nterm == 6)
-      kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 6, kOut>
-            : (order % 4 == 0) ? k_oscprob_batch_pt<4, 6, kOut>
-            : (order % 3 == 0) ? k_oscprob_batch_pt<3, 6, kOut>
-                               : k_oscprob_batch_pt<4, 6, kOut>;
+      kpt = (order % 5 == 0)   ? k_oscprob_batch_pt<5, 6, kOut, kMixed>
+            : (order % 4 == 0) ? k_oscprob_batch_pt<4, 6, kOut, kMixed>
+            : (order % 3 == 0) ? k_oscprob_batch_pt<3, 6, kOut, kMixed>
+                               : k_oscprob_batch_pt<4, 6, kOut, kMixed>;
+#if GNA_BATCH_PT_MIXED_N10
+    if (kMixed && order % 10 == 0)
+      kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed> : k_oscprob_batch_pt<10, 6, kOut, kMixed>;
+#endif
 #if GNA_BATCH_PT_N10
-    if (order % 10 == 0) kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut> : k_oscprob_batch_pt<10, 6, kOut>;
+    if (order % 10 == 0)
+      kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed> : k_oscprob_batch_pt<10, 6, kOut, kMixed>;
 #endif
     const int64_t ng = (pts->npoints + 31) / 32;
     const size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);

@@ -479,6 +479,12 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #ifndef GNA_BATCH_PT_MUNROLL
 #define GNA_BATCH_PT_MUNROLL 1
 #endif
+#ifndef GNA_BATCH_PT_MIXED
+#define GNA_BATCH_PT_MIXED 1  // the mixed tier also takes the points-across-lanes kernel
+#endif
+#ifndef GNA_BATCH_PT_MIXED_N10
+#define GNA_BATCH_PT_MIXED_N10 1
+#endif
 #ifndef GNA_BATCH_PT_N10
 #define GNA_BATCH_PT_N10 0
 #endif
@@ -486,9 +492,9 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #define GNA_BATCH_PT_MIN_POINTS 256
 #endif
 
-template <int N, int NT>
+template <int N, int NT, bool kMixed>
 __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&cw)[NT],
-                                         const double* __restrict__ sE,
+                                         const float (&wf)[NT], const double* __restrict__ sE,
                                          const double* __restrict__ sH, int b, int i, double& A) {
   double iE[N], a[N];
 #pragma unroll
@@ -496,32 +502,56 @@ __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&
     iE[n] = sE[(i + n) * 32 + b];
     a[n] = 0.0;
   }
+  if constexpr (kMixed) {
+    // NEXT-3 mixed tier, as in batch_nodes: kq[] holds kq/2, the node pairs share FFMA2s
+    constexpr int NP = N / 2;
+    gna::f32x2 acc2[NP > 0 ? NP : 1];
+    float acc1 = 0.0f;
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
+    for (int k = 0; k < NP; ++k) acc2[k] = 0ull;
 #pragma unroll
-    for (int n = 0; n < N; ++n) a[n] = fma(cw[j], gna::sin2c(kq[j], iE[n]), a[n]);
+    for (int j = 0; j < NT; ++j) {
+      const gna::f32x2 w2 = gna::f2_pack(wf[j], wf[j]);
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        acc2[k] = gna::f2_fma(w2, gna::cos2_w2(gna::mixed_h2(kq[j], iE[2 * k], kq[j], iE[2 * k + 1])),
+                              acc2[k]);
+      if constexpr (N & 1) acc1 = fmaf(wf[j], gna::cos2_w(gna::mixed_h1(kq[j], iE[N - 1])), acc1);
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      a[2 * k] = (double)gna::f2_lo(acc2[k]);
+      a[2 * k + 1] = (double)gna::f2_hi(acc2[k]);
+    }
+    if constexpr (N & 1) a[N - 1] = (double)acc1;
+  } else {
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+#pragma unroll
+      for (int n = 0; n < N; ++n) a[n] = fma(cw[j], gna::sin2c(kq[j], iE[n]), a[n]);
+    }
   }
 #pragma unroll
   for (int n = 0; n < N; ++n) A = fma(sH[(i + n) * 32 + b], a[n], A);
 }
 
-template <int N, int NT>
+template <int N, int NT, bool kMixed>
 __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const double (&cw)[NT],
-                                        const double* __restrict__ sE,
+                                        const float (&wf)[NT], const double* __restrict__ sE,
                                         const double* __restrict__ sH, int b, int i, double& A) {
   if constexpr (N > 1) {
     if (r == N - 1) {
-      pt_nodes<N - 1, NT>(kq, cw, sE, sH, b, i, A);
+      pt_nodes<N - 1, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
       return;
     }
-    pt_tail<N - 1, NT>(r, kq, cw, sE, sH, b, i, A);
+    pt_tail<N - 1, NT, kMixed>(r, kq, cw, wf, sE, sH, b, i, A);
   }
 }
 
 // A tile may be split into S = 2^(5 - lv) sub-tiles of 2^lv consecutive visits (more,
 // shorter warps: a smaller last wave); each sub-tile's tree sum is a chi2 sub-partial and
 // k_chi2_reduce<S> finishes the tree's top levels.
-template <int N, int NT, int kOut>
+template <int N, int NT, int kOut, bool kMixed = false>
 __global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
     int order, int64_t nbins, int64_t npoints, int64_t bpp, int lv, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
@@ -559,11 +589,13 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
     sW[lane] = W;
   }
   double kq[NT], cw[NT];
+  float wf[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     const double2 c = w.coef[pp * NT + j];
-    kq[j] = c.x;
+    kq[j] = kMixed ? 0.5 * c.x : c.x;  // mixed tier: kq/2 (exact), weights in fp32
     cw[j] = c.y;
+    wf[j] = __double2float_rn(c.y);
   }
   const double c0 = w.c0[pp];
   __syncwarp();
@@ -579,8 +611,8 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
     const int b = (int)(__brev((unsigned)m) >> 27);
     double A = 0.0;
     int i = 0;
-    for (; i + N <= order; i += N) pt_nodes<N, NT>(kq, cw, sE, sH, b, i, A);
-    if (i < order) pt_tail<N, NT>(order - i, kq, cw, sE, sH, b, i, A);
+    for (; i + N <= order; i += N) pt_nodes<N, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
+    if (i < order) pt_tail<N, NT, kMixed>(order - i, kq, cw, wf, sE, sH, b, i, A);
     const double s = fma(c0, sW[b], -A);
     x2 = 0.0;
     // bins past the end of a ragged tile are computed and dropped: skipping them with a

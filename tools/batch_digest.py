@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--lib", default=None)
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--points", type=int, default=0, help="first N points only (0 = all)")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
     a = ap.parse_args()
     gna.load(a.lib)
     c = synth.config(a.workload)
@@ -31,11 +32,12 @@ def main():
     sp, x2 = gna.oscprob_batch(t, c["L_km"], c["omega"],
                                torch.tensor(c["edges"], dtype=torch.float64, device=dev),
                                c["order"], data=torch.tensor(c["data"], dtype=torch.float64,
-                                                             device=dev))
+                                                             device=dev),
+                               precision=a.precision)
     torch.cuda.synchronize()
     hs = hashlib.sha256(sp.cpu().numpy().tobytes()).hexdigest()[:16]
     hx = hashlib.sha256(x2.cpu().numpy().tobytes()).hexdigest()[:16]
-    print("%s %s points=%d spectra=%s chi2=%s" % (a.lib or "default", a.workload,
+    print("%s %s %s points=%d spectra=%s chi2=%s" % (a.lib or "default", a.workload, a.precision,
                                                   sp.shape[0], hs, hx))
 
 

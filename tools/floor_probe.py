@@ -52,6 +52,14 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     print("empty event pair        plain %.2f us  backed %.2f us" % (
         timeit(lambda: None, flush, False), timeit(lambda: None, flush, True)))
+    # an empty kernel (torch's spin kernel with 0 cycles) and a 1-element fill, graph-replayed
+    tiny = torch.empty(1, dtype=torch.float64, device=dev)
+    for name, fn in (("empty kernel", lambda: torch.cuda._sleep(0)),
+                     ("1-element fill", lambda: tiny.fill_(1.0))):
+        fn()
+        g = graph_of(fn)
+        print("%-22s  graph backed %.2f us  eager backed %.2f us" % (
+            name, timeit(g.replay, flush, True), timeit(fn, flush, True)))
     for nbins in (1, 100_000, 1_000_000):
         edges = torch.tensor(synth.uniform_edges(nbins), dtype=torch.float64, device=dev)
         out = torch.empty(nbins, dtype=torch.float64, device=dev)
