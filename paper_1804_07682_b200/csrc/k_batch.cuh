@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #define GNA_BATCH_PT 1
 #endif
 #ifndef GNA_BATCH_PT_MINB
-#define GNA_BATCH_PT_MINB 1
+#define GNA_BATCH_PT_MINB 24  // <= 80 registers: 24 warps per SM
 #endif
 #ifndef GNA_BATCH_PT_SUB
 #define GNA_BATCH_PT_SUB 2  // sub-tiles per 32-bin tile: 1, 2 or 4
@@ -548,6 +548,51 @@ __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const dou
   }
 }
 
+// One (sub-)tile of k_oscprob_batch_pt: the bins of visits [sub 2^lv, (sub + 1) 2^lv) in
+// bit-reversed order.  chi2 partial of the tile = xor tree over its 32 bins (k_oscprob_batch);
+// visited in bit-reversed order the tree pairs consecutive visits: r[l] holds the pending
+// left operand of level l, and after the sub-tile's last visit x2 is its subtree sum.
+// kRagged: bins at or past nbins are skipped (x2 = 0 for them, as in k_oscprob_batch).
+template <bool kRagged, int N, int NT, int kOut, bool kMixed>
+__device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (&cw)[NT],
+                                          const float (&wf)[NT], double c0,
+                                          const double* __restrict__ sE,
+                                          const double* __restrict__ sH,
+                                          const double* __restrict__ sW,
+                                          const double* __restrict__ sD,
+                                          const double* __restrict__ sID, int order, int64_t k0,
+                                          int64_t nbins, double* __restrict__ out, bool pact,
+                                          int sub, int lv) {
+  double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double x2 = 0.0;
+  const int m0 = sub << lv;
+  GNA_UNROLL(GNA_BATCH_PT_MUNROLL)
+  for (int m = m0; m < m0 + (1 << lv); ++m) {
+    const int b = (int)(__brev((unsigned)m) >> 27);
+    x2 = 0.0;
+    if (!kRagged || k0 + b < nbins) {
+      double A = 0.0;
+      int i = 0;
+      for (; i + N <= order; i += N) pt_nodes<N, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
+      if (i < order) pt_tail<N, NT, kMixed>(order - i, kq, cw, wf, sE, sH, b, i, A);
+      const double s = fma(c0, sW[b], -A);
+      if (out && pact) out_store<kOut>(out + k0 + b, s);
+      const double d = s - sD[b];
+      x2 = d * d * sID[b];
+    }
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      if (l >= lv) break;
+      if (!(m & (1 << l))) {
+        r[l] = x2;
+        break;
+      }
+      x2 = r[l] + x2;
+    }
+  }
+  return x2;
+}
+
 // A tile may be split into S = 2^(5 - lv) sub-tiles of 2^lv consecutive visits (more,
 // shorter warps: a smaller last wave); each sub-tile's tree sum is a chi2 sub-partial and
 // k_chi2_reduce<S> finishes the tree's top levels.
@@ -599,39 +644,15 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
   }
   const double c0 = w.c0[pp];
   __syncwarp();
-  // chi2 partial of the tile = xor tree over its 32 bins (k_oscprob_batch); visited in
-  // bit-reversed order the tree pairs consecutive visits: r[l] holds the pending left
-  // operand of level l, and after the sub-tile's last visit x2 is its subtree sum
-  double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  double x2 = 0.0;
   double* __restrict__ out = spectra ? spectra + pp * nbins : nullptr;
-  const int m0 = sub << lv;
-  GNA_UNROLL(GNA_BATCH_PT_MUNROLL)
-  for (int m = m0; m < m0 + (1 << lv); ++m) {
-    const int b = (int)(__brev((unsigned)m) >> 27);
-    double A = 0.0;
-    int i = 0;
-    for (; i + N <= order; i += N) pt_nodes<N, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
-    if (i < order) pt_tail<N, NT, kMixed>(order - i, kq, cw, wf, sE, sH, b, i, A);
-    const double s = fma(c0, sW[b], -A);
-    x2 = 0.0;
-    // bins past the end of a ragged tile are computed and dropped: skipping them with a
-    // warp-uniform branch measured 1 % slower on cfg4 (357.5 vs 361.7 G/s)
-    if (k0 + b < nbins) {
-      if (out && pact) out_store<kOut>(out + k0 + b, s);
-      const double d = s - sD[b];
-      x2 = d * d * sID[b];
-    }
-#pragma unroll
-    for (int l = 0; l < 5; ++l) {
-      if (l >= lv) break;
-      if (!(m & (1 << l))) {
-        r[l] = x2;
-        break;
-      }
-      x2 = r[l] + x2;
-    }
-  }
+  // a ragged last tile (nbins not a multiple of 32) skips its empty bins in a separate copy
+  // of the loop, so full tiles run the branch-free one
+  const double x2 =
+      k0 + 32 <= nbins
+          ? pt_tile<false, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+                                                nbins, out, pact, sub, lv)
+          : pt_tile<true, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+                                               nbins, out, pact, sub, lv);
   if (w.partial && pact) w.partial[(p * warps_per_point_dev(nbins) + wt) * S + sub] = x2;
   if constexpr (kOut != kOutLocal) __threadfence_system();
 }
