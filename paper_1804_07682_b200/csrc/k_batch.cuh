@@ -482,6 +482,9 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #ifndef GNA_BATCH_PT_MIXED
 #define GNA_BATCH_PT_MIXED 1  // the mixed tier also takes the points-across-lanes kernel
 #endif
+#ifndef GNA_BATCH_PT_MIXED_MINB
+#define GNA_BATCH_PT_MIXED_MINB 1  // 72 registers; a cap of 64 (32 warps per SM) lost 3 %
+#endif
 #ifndef GNA_BATCH_PT_MIXED_N10
 #define GNA_BATCH_PT_MIXED_N10 1
 #endif
@@ -552,8 +555,10 @@ __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const dou
 // bit-reversed order.  chi2 partial of the tile = xor tree over its 32 bins (k_oscprob_batch);
 // visited in bit-reversed order the tree pairs consecutive visits: r[l] holds the pending
 // left operand of level l, and after the sub-tile's last visit x2 is its subtree sum.
-// kRagged: bins at or past nbins are skipped (x2 = 0 for them, as in k_oscprob_batch).
-template <bool kRagged, int N, int NT, int kOut, bool kMixed>
+// kMode 0: a full tile (no bounds checks); 1: bins at or past nbins are skipped; 2: every
+// bin is computed and those at or past nbins are dropped (x2 = 0 for them in both cases, as
+// in k_oscprob_batch).
+template <int kMode, int N, int NT, int kOut, bool kMixed>
 __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (&cw)[NT],
                                           const float (&wf)[NT], double c0,
                                           const double* __restrict__ sE,
@@ -570,15 +575,17 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
   for (int m = m0; m < m0 + (1 << lv); ++m) {
     const int b = (int)(__brev((unsigned)m) >> 27);
     x2 = 0.0;
-    if (!kRagged || k0 + b < nbins) {
+    if (kMode != 1 || k0 + b < nbins) {
       double A = 0.0;
       int i = 0;
       for (; i + N <= order; i += N) pt_nodes<N, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
       if (i < order) pt_tail<N, NT, kMixed>(order - i, kq, cw, wf, sE, sH, b, i, A);
       const double s = fma(c0, sW[b], -A);
-      if (out && pact) out_store<kOut>(out + k0 + b, s);
-      const double d = s - sD[b];
-      x2 = d * d * sID[b];
+      if (kMode != 2 || k0 + b < nbins) {
+        if (out && pact) out_store<kOut>(out + k0 + b, s);
+        const double d = s - sD[b];
+        x2 = d * d * sID[b];
+      }
     }
 #pragma unroll
     for (int l = 0; l < 5; ++l) {
@@ -597,7 +604,8 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
 // shorter warps: a smaller last wave); each sub-tile's tree sum is a chi2 sub-partial and
 // k_chi2_reduce<S> finishes the tree's top levels.
 template <int N, int NT, int kOut, bool kMixed = false>
-__global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
+__global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BATCH_PT_MINB)
+    k_oscprob_batch_pt(
     int order, int64_t nbins, int64_t npoints, int64_t bpp, int lv, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double s_pt[];
@@ -645,13 +653,19 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PT_MINB) k_oscprob_batch_pt(
   const double c0 = w.c0[pp];
   __syncwarp();
   double* __restrict__ out = spectra ? spectra + pp * nbins : nullptr;
-  // a ragged last tile (nbins not a multiple of 32) skips its empty bins in a separate copy
-  // of the loop, so full tiles run the branch-free one
-  const double x2 =
-      k0 + 32 <= nbins
-          ? pt_tile<false, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
-                                                nbins, out, pact, sub, lv)
-          : pt_tile<true, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+  // fp64: a ragged last tile (nbins not a multiple of 32) skips its empty bins in a separate
+  // copy of the loop, so full tiles run the branch-free one (cfg4 363.0 -> 364.2 G/s).  Mixed
+  // tier: one loop that computes every bin and drops the empty ones — the second loop copy
+  // cost it 7 % (556 -> 518 G/s).
+  double x2;
+  if constexpr (kMixed)
+    x2 = pt_tile<2, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0, nbins,
+                                         out, pact, sub, lv);
+  else
+    x2 = k0 + 32 <= nbins
+             ? pt_tile<0, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+                                               nbins, out, pact, sub, lv)
+             : pt_tile<1, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
                                                nbins, out, pact, sub, lv);
   if (w.partial && pact) w.partial[(p * warps_per_point_dev(nbins) + wt) * S + sub] = x2;
   if constexpr (kOut != kOutLocal) __threadfence_system();

@@ -33,7 +33,7 @@ WORKLOADS = ["cfg5", "cfg4", "cfg3", "cfg2", "cfg1", "cfg4grid", "cfg3emu", "cfg
 CAPTURES = {
     "batch": ("cfg5", "k_oscprob_batch"),
     "batch_pt": ("cfg4", "k_oscprob_batch_pt"),
-    "batch_pi_mixed": ("cfg4_mixed", "k_oscprob_batch_pi<..., kMixed>"),
+    "batch_pt_mixed": ("cfg4_mixed", "k_oscprob_batch_pt<..., kMixed>"),
     "eval": ("cfg3", "k_oscprob_eval_tma"),
     "eval_ab": ("cfg3emu", "k_oscprob_eval_tma<PabCoef>"),
     "gl": ("cfg2", "k_gl_integrate"),

@@ -29,7 +29,7 @@ prof() {  # name workload kernel-regex [extra bench args]; PROFS="a b" limits th
 }
 prof batch cfg5 '^k_oscprob_batch$'
 prof batch_pt cfg4 k_oscprob_batch_pt
-prof batch_pi_mixed cfg4 k_oscprob_batch_pi "--precision mixed"
+prof batch_pt_mixed cfg4 k_oscprob_batch_pt "--precision mixed"
 prof eval cfg3 k_oscprob_eval_tma
 prof eval_ab cfg3emu k_oscprob_eval_tma
 prof gl cfg2 k_gl_integrate
