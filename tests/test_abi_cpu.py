@@ -373,3 +373,27 @@ def test_kernel_sin2_small_phase_error_vanishes():
             p = _fma(p, u, c)
         ref = -mp.cos(mp.pi * mp.mpf(float(f))) / 2
         assert abs(float(p - ref)) <= 1.2e-16 * (1 + 1e6 * u)
+
+
+def compile_c_example(out_path):
+    """Build examples/gl_integrate.c: include/gna_b200.h must be valid C11 and the library
+    must link from plain C (no torch, no Python)."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_1804_07682_b200")
+    cuda = "/usr/local/cuda"
+    cmd = ["gcc", "-std=c11", "-O2", "-Wall", "-Wextra", "-Werror",
+           "-I" + os.path.join(root, "include"), "-I" + os.path.join(cuda, "include"),
+           os.path.join(root, "examples", "gl_integrate.c"), "-L" + pkg, "-lgna_b200",
+           "-L" + os.path.join(cuda, "lib64"), "-lcudart", "-lm", "-Wl,-rpath," + pkg,
+           "-o", str(out_path)]
+    subprocess.check_call(cmd)
+    return str(out_path)
+
+
+def test_c_abi_example_compiles_and_links(lib, tmp_path):
+    import shutil
+    if shutil.which("gcc") is None or not os.path.exists("/usr/local/cuda/include/cuda_runtime_api.h"):
+        pytest.skip("gcc or the CUDA headers are not available")
+    exe = compile_c_example(tmp_path / "gl_integrate_c")
+    assert os.path.exists(exe)

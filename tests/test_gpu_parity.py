@@ -822,3 +822,15 @@ def test_launch_count_increments(gna):
     n0 = gna.launch_count()
     gna.gl_integrate(synth.CANONICAL, 52.5, _t(synth.uniform_edges(10)), 5)
     assert gna.launch_count() == n0 + 1
+
+
+def test_c_abi_example_runs(gna, tmp_path):
+    """examples/gl_integrate.c: the ABI from plain C (cudaMalloc'd buffers, gna_gl_integrate,
+    gna_gl_integrate_host, EINVAL checks) exits 0."""
+    import subprocess
+
+    from test_abi_cpu import compile_c_example
+    exe = compile_c_example(tmp_path / "gl_integrate_c")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.strip().endswith("ok")
