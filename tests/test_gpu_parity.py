@@ -480,6 +480,26 @@ def test_batch_points_across_lanes_path_vs_oracle_and_bitwise(gna, nbase, nbins,
     assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
+@pytest.mark.parametrize("nbase,nbins,order", [(1, 257, 7), (2, 300, 5), (1, 100, 10),
+                                               (2, 33, 32), (1, 1, 1)])
+def test_batch_mixed_points_across_lanes_vs_oracle_and_bitwise(gna, nbase, nbins, order):
+    """Mixed tier with >= 256 points and <= 2 baselines: the points-across-lanes kernel with
+    packed node pairs (odd groups end in a scalar chain).  Sampled parity at the tier
+    tolerance, and bitwise equality with the points-inner mixed kernel (100-point calls)."""
+    g = synth.rng(1700 + nbase * nbins + order)
+    pts, L, om, edges, data = _batch_case(g, 411, nbase, nbins, order)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data, precision="mixed")
+    idx = np.array([0, 33, 205, 410])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_MIXED
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound_tol(spr, data, TOL_MIXED))
+    for lo, hi in ((0, 100), (100, 411)):
+        s2 = synth.subset_points(pts, np.arange(lo, hi))
+        sps, x2s = _run_batch(gna, s2, L, om, edges, order, data, precision="mixed")
+        assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi]), (lo, hi)
+
+
 def test_batch_single_baseline_matches_gl_integrate(gna):
     g = synth.rng(41)
     pts, _, _, edges, _ = _batch_case(g, 4, 1, 200, 10)
