@@ -284,7 +284,10 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            # the same label as this workload's own arm (the batch configs split a fixed set
+            # of parameter points over the ranks)
+            "scaling": "strong" if args.workload in ("cfg4", "cfg5") else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": c["desc"],
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "oracle",
                              "sample": sample},
