@@ -280,6 +280,9 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   // mixed tier: 10 nodes (5 packed pairs) per coefficient load when the order allows
   if (kMixed && order % 10 == 0) kern = k_oscprob_batch<kBatchWarps, 10, kOut, kMixed>;
 #endif
+#if GNA_BATCH_N10_FP64
+  if (!kMixed && order % 10 == 0) kern = k_oscprob_batch<kBatchWarps, 10, kOut, kMixed>;
+#endif
   int pt_sub = 1;  // chi2 sub-partials per tile (k_oscprob_batch_pt)
   if ((GNA_BATCH_PT_MIXED || !kMixed) && GNA_BATCH_PT && kBatchWarps == 1 &&
       (nterm == 3 || nterm == 6) && pts->npoints >= GNA_BATCH_PT_MIN_POINTS) {
