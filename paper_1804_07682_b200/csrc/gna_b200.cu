@@ -730,13 +730,15 @@ int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbas
   void* bws = w;
   const gna_param_batch pts = {cand, cand + kFitCand, cand + 2 * kFitCand, cand + 3 * kFitCand,
                                kFitCand};
-  for (int it = 0; it < niter; ++it) {
+  if (niter > 0) {
     k_fit_candidates<<<1, 128, 0, s>>>(d_state, cand);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  for (int it = 0; it < niter; ++it) {
     if ((rc = launch_batch(&pts, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data,
                            chi2, bws, s)))
       return rc;
-    k_fit_update<<<1, 128, 0, s>>>(d_state, cand, chi2, d_hist, it);
+    k_fit_update<<<1, 128, 0, s>>>(d_state, cand, chi2, d_hist, it, it + 1 < niter);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e);

@@ -15,11 +15,9 @@ namespace {
 constexpr int kFitDim = 4;
 constexpr int kFitCand = 81;  // 3^4
 
-// state = {centre[4], step[4]} (device, fp64)
-__global__ void __launch_bounds__(128) k_fit_candidates(const double* __restrict__ state,
-                                                        double* __restrict__ cand) {
-  const int c = threadIdx.x;
-  if (c >= kFitCand) return;
+// state = {centre[4], step[4]} (device, fp64); candidate c of the current state
+__device__ __forceinline__ void fit_candidate(const double* __restrict__ state,
+                                              double* __restrict__ cand, int c) {
   int code = c;
 #pragma unroll
   for (int d = 0; d < kFitDim; ++d) {
@@ -29,10 +27,19 @@ __global__ void __launch_bounds__(128) k_fit_candidates(const double* __restrict
   }
 }
 
+// the first iteration's candidates (later ones are written by k_fit_update)
+__global__ void __launch_bounds__(128) k_fit_candidates(const double* __restrict__ state,
+                                                        double* __restrict__ cand) {
+  if (threadIdx.x < kFitCand) fit_candidate(state, cand, threadIdx.x);
+}
+
+// argmin + move/halve, then (next_cand) the next iteration's candidates from the new state:
+// one launch per iteration fewer than a separate candidates kernel
 __global__ void __launch_bounds__(128) k_fit_update(double* __restrict__ state,
-                                                    const double* __restrict__ cand,
+                                                    double* __restrict__ cand,
                                                     const double* __restrict__ chi2,
-                                                    double* __restrict__ hist, int iter) {
+                                                    double* __restrict__ hist, int iter,
+                                                    int next_cand) {
   __shared__ double s_v[128];
   __shared__ int s_i[128];
   const int t = threadIdx.x;
@@ -60,6 +67,10 @@ __global__ void __launch_bounds__(128) k_fit_update(double* __restrict__ state,
       for (int d = 0; d < kFitDim; ++d) state[d] = cand[d * kFitCand + best];
     }
     if (hist) hist[iter] = fmin(s_v[0], chi2[centre]);
+  }
+  if (next_cand) {
+    __syncthreads();  // thread 0's state update (and its reads of cand) are complete
+    if (t < kFitCand) fit_candidate(state, cand, t);
   }
 }
 
