@@ -804,6 +804,39 @@ def test_fit_pattern_search_recovers_truth(gna):
     assert np.all(np.abs(x - truth) <= 1e-6 * np.abs(truth)), (x, truth)
 
 
+def test_fit_pattern_search_steps_match_host_compass_search_on_oracle_chi2(gna):
+    """Each GPU iteration (niter = 1 calls) equals one compass step computed on the host:
+    the 81 candidates centre + step * {-1, 0, 1}^4 (first coordinate fastest), their chi^2 from
+    the oracle, argmin with ties to the lowest index; move there if it beats the centre, else
+    halve the steps.  The state after every step must match bit for bit."""
+    truth, L, om, edges, data = _fit_case()
+    step = np.array([0.01, 0.005, 2e-6, 5e-5])
+    st = np.r_[truth + np.array([0.7, -0.6, 0.8, -0.5]) * step, step]
+    de, dd = _t(edges), _t(data)
+    offs = np.array([[(c // 3 ** d) % 3 - 1 for d in range(4)] for c in range(81)], dtype=float)
+    moved = halved = 0
+    for _ in range(6):
+        gpu = _t(st)
+        hist = _np(gna.fit_pattern_search(gpu, L, om, de, 5, dd, 1))
+        cand = st[:4][None, :] + offs * st[4:][None, :]
+        pts = dict(theta12=cand[:, 0], theta13=cand[:, 1], dm2_21=cand[:, 2], dm2_31=cand[:, 3])
+        _, x2 = oracle.batch(pts, L, om, edges, 5, data=data, want_spectra=False, nthreads=_nt())
+        best = int(np.argmin(x2))
+        gaps = np.sort(np.unique(x2))
+        assert gaps.size < 2 or gaps[1] - gaps[0] > 1e-9 * gaps[1]  # decision not at the tolerance
+        new = st.copy()
+        if best != 40 and x2[best] < x2[40]:
+            new[:4] = cand[best]
+            moved += 1
+        else:
+            new[4:] *= 0.5
+            halved += 1
+        assert np.array_equal(_np(gpu), new)
+        assert abs(hist[0] - min(x2[best], x2[40])) <= 1e-9 * x2[40]
+        st = new
+    assert moved and halved
+
+
 def test_fit_pattern_search_deterministic_and_graph_capturable(gna):
     import torch
     truth, L, om, edges, data = _fit_case()
