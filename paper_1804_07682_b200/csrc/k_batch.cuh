@@ -464,12 +464,14 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 // = one warp = 32 consecutive points x one 32-bin tile.  Each lane keeps its point's NT
 // coefficients in registers; the tile's node tables (1/E, h w), W, D and 1/D are staged once
 // into shared memory and read back as warp-uniform broadcasts, bin by bin.  Compared with
-// k_oscprob_batch_pi this drops the per-bin chi2 shuffle tree and the idle lanes of the
-// ragged last bin tile (nbins = 1000 = 31.25 tiles), and the per-point shared-memory
-// accumulators.  Results are bitwise identical to k_oscprob_batch: the same operations in
-// the same order per (point, bin), and the tile's chi2 partial is the same xor-tree sum —
-// the bins are visited in bit-reversed order, which turns the tree into consecutive pairs,
-// summed online with a 5-level binary counter.
+// k_oscprob_batch_pi this drops the per-bin chi2 shuffle tree, the per-point shared-memory
+// accumulators and (fp64) the empty bins of a ragged last tile (nbins = 1000 = 31.25
+// tiles).  Results are bitwise identical to k_oscprob_batch: the same operations in the
+// same order per (point, bin), and the tile's chi2 partial is the same xor-tree sum — the
+// bins are visited in bit-reversed order, which turns the tree into consecutive pairs,
+// summed online with a 5-level binary counter (pt_tile).  The mixed tier runs the same
+// kernel with the NEXT-3 arithmetic of batch_nodes (node pairs on packed FFMA2s).
+// §6.2 has the measurements behind each choice.
 #ifndef GNA_BATCH_PT
 #define GNA_BATCH_PT 1
 #endif
