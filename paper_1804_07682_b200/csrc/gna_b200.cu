@@ -409,7 +409,7 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
 template <class Coef>
 int launch_gl(const Coef& c, const double* edges, int64_t nbins, int order, double* bins,
               cudaStream_t s) {
-  if (nbins >= (int64_t)GNA_GL_TB_MIN_BINS) {
+  if (nbins >= gl_tb_min_bins<Coef>()) {
     // thread per bin, GL table as uniform constant-bank operands (k_gl.cuh)
     const int64_t grid = (nbins + kGLTbThreads - 1) / kGLTbThreads;
     if (grid > 0x7fffffffLL) return GNA_EINVAL;

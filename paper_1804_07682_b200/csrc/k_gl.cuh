@@ -1,6 +1,7 @@
 // k_gl.cuh — (a3)+(a4) single-point Gauss-Legendre kernel
 // Part of libgna_b200.so: included once, from gna_b200.cu (single translation unit).
 #pragma once
+#include <type_traits>
 #include <utility>
 
 #include "gna_common.cuh"
@@ -63,9 +64,26 @@ __global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Co
 #ifndef GNA_GL_TB_MINB
 #define GNA_GL_TB_MINB 4
 #endif
+// nbins from which the thread-per-bin kernel is used, per coefficient type (below: lane
+// pairs).  Back-to-back launch times, tools/gl_b2b.py (profiles/r01_gl_b2b.jsonl): P_ee fp64
+// is faster (or equal) with thread per bin at every size from 1 bin up (cfg1 1.79 -> 1.54 us,
+// cfg2 4.76 -> 4.53 us); the mixed tier and the general channel are faster with lane pairs
+// up to ~10^5 bins and with thread per bin at 10^6.
 #ifndef GNA_GL_TB_MIN_BINS
-#define GNA_GL_TB_MIN_BINS 32768  // below: lane pairs (latency); above: thread per bin
+#define GNA_GL_TB_MIN_BINS 1
 #endif
+#ifndef GNA_GL_TB_MIN_BINS_MIXED
+#define GNA_GL_TB_MIN_BINS_MIXED 131072
+#endif
+#ifndef GNA_GL_TB_MIN_BINS_AB
+#define GNA_GL_TB_MIN_BINS_AB 262144
+#endif
+template <class Coef>
+constexpr int64_t gl_tb_min_bins() {
+  return std::is_same<Coef, gna::PeeCoef>::value       ? (int64_t)GNA_GL_TB_MIN_BINS
+         : std::is_same<Coef, gna::PeeMixCoef>::value ? (int64_t)GNA_GL_TB_MIN_BINS_MIXED
+                                                       : (int64_t)GNA_GL_TB_MIN_BINS_AB;
+}
 #ifndef GNA_GL_TB_THREADS
 #define GNA_GL_TB_THREADS 128
 #endif

@@ -304,6 +304,25 @@ def test_gl_thread_per_bin_path_all_group_shapes(gna, order):
     assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
 
 
+@pytest.mark.parametrize("mode", ["mixed", "ab"])
+def test_gl_bin_value_independent_of_nbins_across_kernels(gna, mode):
+    """The lane-pair kernel (small nbins) and the thread-per-bin kernel (large nbins) form a
+    bin's value identically: 300 000 bins in one call equal the same edges in 1 000-bin
+    calls, bit for bit (mixed tier and general channel, which switch kernels by nbins)."""
+    g = synth.rng(1900)
+    p = synth.random_params(g)
+    edges = np.sort(g.uniform(1.0, 10.0, 300_001))
+    de = _t(edges)
+
+    def run(e):
+        if mode == "ab":
+            return _np(gna.gl_integrate_ab(0, 1, p, 60.0, e, 10))
+        return _np(gna.gl_integrate(p, 60.0, e, 10, precision="mixed"))
+    full = run(de)
+    parts = np.concatenate([run(de[k:k + 1001]) for k in range(0, 300_000, 1000)])
+    assert np.array_equal(full, parts)
+
+
 def test_gl_zero_mixing_is_bin_width(gna):
     e = synth.uniform_edges(333, 1.0, 10.0)
     p0 = dict(synth.CANONICAL, theta12=0.0, theta13=0.0)
