@@ -292,7 +292,7 @@ def test_gl_ragged_sizes(gna, nbins):
 
 @pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 7, 10, 11, 13, 16, 29, 32])
 def test_gl_thread_per_bin_path_all_group_shapes(gna, order):
-    # nbins above GNA_GL_TB_MIN_BINS (32768): the thread-per-bin kernel, node groups of
+    # fp64 P_ee runs the thread-per-bin kernel at every nbins (gl_tb_min_bins); node groups of
     # 5/4/3 and the ragged last group (orders 7, 11, 13, 29)
     g = synth.rng(1300 + order)
     p = synth.random_params(g)
