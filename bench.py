@@ -75,6 +75,10 @@ def parse():
                          "one GPU, with GNA_BENCH_SAME_DEVICE=1; not for measurements)")
     ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "fused"],
                     help="N>1 exchange: fused kernel-epilogue stores (validated) or NCCL all-gather")
+    ap.add_argument("--fused-probe", action="store_true",
+                    help=argparse.SUPPRESS)  # internal: the isolated start-up check (N > 1)
+    ap.add_argument("--probe-timeout", type=float, default=240.0,
+                    help="seconds allowed for the isolated fused-gather start-up check")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as a CUDA graph (auto: when N == 1)")
     a = ap.parse_args()
@@ -370,15 +374,142 @@ def _cpu_model():
     return None
 
 
+def auto_chunks(npoints: int, world: int, evals_per_point: int) -> int:
+    """Gather pipeline depth for N > 1: one chunk per ~1e8 energy points of
+    the rank's shard (>= ~0.25 ms of kernel, i.e. many waves per chunk), 1 to 4 chunks."""
+    if world == 1:
+        return 1
+    per_rank = -(-npoints // world) * evals_per_point
+    return int(max(1, min(4, round(per_rank / 1e8))))
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def isolated_fused_probe(args, world, rank, dist):
+    """Rank 0 runs the fused-epilogue start-up check (bench.py --fused-probe) as a separate
+    N-rank torch.distributed.run job with a hard timeout, while the other ranks wait on the
+    store (CPU side, no GPU work).  Returns {"ok": bool, "mode"/"why": str}."""
+    store = dist.distributed_c10d._get_default_store()
+    key = "gna_fused_probe"
+    if rank == 0:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+               str(world), "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+               os.path.abspath(__file__), "--fused-probe", "--gpus", str(world), "--workload",
+               args.workload, "--precision", args.precision]
+        env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC")
+               and k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE",
+                             "GROUP_RANK", "ROLE_RANK", "ROLE_WORLD_SIZE", "MASTER_ADDR",
+                             "MASTER_PORT", "TORCHELASTIC_RUN_ID")}
+        res = {"ok": False, "why": "probe did not run"}
+        t0 = time.time()
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, env=env,
+                                 timeout=args.probe_timeout)
+            ok_lines = [l for l in out.stdout.splitlines() if l.startswith("FUSED_PROBE_OK")]
+            if out.returncode == 0 and ok_lines:
+                res = {"ok": True, "mode": ok_lines[-1].split()[1]}
+            else:
+                tail = (out.stdout + out.stderr).strip().splitlines()[-1:] or ["no output"]
+                res = {"ok": False, "why": "probe rc=%d: %s" % (out.returncode, tail[0][:160])}
+        except subprocess.TimeoutExpired:
+            res = {"ok": False, "why": "probe timed out after %.0f s" % args.probe_timeout}
+        except OSError as exc:
+            res = {"ok": False, "why": "probe failed to start: %s" % exc}
+        res["seconds"] = round(time.time() - t0, 1)
+        store.set(key, json.dumps(res))
+        return res
+    store.wait([key], __import__("datetime").timedelta(seconds=args.probe_timeout + 120))
+    return json.loads(store.get(key))
+
+
+def fused_probe_main(args):
+    """--fused-probe (one rank of the isolated check): build the symmetric-memory window, run
+    the batch with the gather fused into its epilogue on a small slice of the workload (every
+    baseline, bin and node; 8 points per rank) and compare the gathered result bit for bit
+    with one local batch over the same points.  Prints FUSED_PROBE_OK <mode> on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_07682_b200 as gna
+    from paper_1804_07682_b200 import dist as gdist
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    try:
+        gna.load(args.lib)
+        c = workload(args.workload)
+        f64 = dict(dtype=torch.float64, device=dev)
+        P = min(c["points"]["theta12"].size, 8 * world)
+        nb = c["edges"].size - 1
+        allp = {k: torch.tensor(v[:P], **f64) for k, v in c["points"].items()}
+        edges, data = torch.tensor(c["edges"], **f64), torch.tensor(c["data"], **f64)
+        fg = gdist.FusedGather(P, nb, dev)
+        sp_ptr, x2_ptr, flags = fg.out_ptrs()
+        if args.precision == "mixed":
+            flags |= gna.GNA_PREC_MIXED
+        mine = {k: v[fg.lo:fg.hi].contiguous() for k, v in allp.items()}
+        fg.spectra.fill_(float("nan"))
+        fg.chi2.fill_(float("nan"))
+        fg.barrier(timeout_ms=20_000)
+        gna.oscprob_batch_ex(mine, c["L_km"], c["omega"], edges, c["order"], sp_ptr, x2_ptr,
+                             flags, data=data)
+        fg.barrier(timeout_ms=20_000)
+        torch.cuda.synchronize()
+        ok = torch.ones(1, device=dev)
+        if rank == 0 or fg.multicast:
+            sp, x2 = gna.oscprob_batch(allp, c["L_km"], c["omega"], edges, c["order"], data=data,
+                                       precision=args.precision)
+            ok.fill_(1.0 if torch.equal(fg.spectra, sp) and torch.equal(fg.chi2, x2) else 0.0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        torch.cuda.synchronize()
+        if float(ok) != 1.0:
+            print("fused probe: gathered result differs from the local batch", file=sys.stderr)
+            return 3
+        if rank == 0:
+            print("FUSED_PROBE_OK %s" % ("multicast" if fg.multicast else "peer-to-root"),
+                  flush=True)
+        return 0
+    finally:
+        dist.destroy_process_group()
+
+
+def relaunch(n: int) -> int:
+    """Re-run this command as n ranks under torch.distributed.run on 127.0.0.1 (one process
+    per GPU); returns the launcher's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 # ----------------------------------------------------------------------------- our arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # N > 1 without a launcher: start the N ranks ourselves (one process per GPU, the
+        # driver's own torchrun command line); rank 0 prints the JSON line
+        sys.exit(relaunch(args.gpus))
+    if args.fused_probe:
+        sys.exit(fused_probe_main(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and world == 1 and args.gpus > 1:
-        print("run N>1 under torchrun (WORLD_SIZE unset)", file=sys.stderr)
-        sys.exit(2)
+    if world != args.gpus:  # the launcher's world size is what runs
+        print("bench.py: --gpus %d under WORLD_SIZE=%d; using %d ranks" % (args.gpus, world, world),
+              file=sys.stderr)
     if args.impl == "reference":
         if args.workload == "cfg5fit":
             args.workload = "cfg5"  # the oracle has no fit loop: time its batch evaluation
@@ -412,7 +543,7 @@ def main():
     if args.workload in ("cfg4", "cfg5"):
         P = c["points"]["theta12"].size
         nb = c["edges"].size - 1
-        chunks = args.chunks or (4 if world > 1 else 1)
+        chunks = args.chunks or auto_chunks(P, world, c["L_km"].size * nb * c["order"])
         sb = gdist.ShardedBatch(P, nb, world, rank, chunks=chunks).allocate(dev)
         lo, hi = sb.lo, sb.hi
         pts = {k: torch.tensor(v[lo:hi], **f64) for k, v in c["points"].items()}
@@ -425,17 +556,28 @@ def main():
         kern_ev = []
 
         def compute(vlo, vhi, sp_rows, x2_rows):
+            # chunks after a step's first reuse its node tables (1/E, h w) in `ws`
             sub = {k: v[vlo:vhi] for k, v in pts.items()}
             with KernelTimer(kern_ev):
                 gna.oscprob_batch(sub, L, om, edges, c["order"], data=data, spectra=sp_rows,
-                                  chi2=x2_rows, workspace=ws, precision=args.precision)
+                                  chi2=x2_rows, workspace=ws, precision=args.precision,
+                                  tables_valid=vlo > 0)
 
         def step():
             sb.step(compute, comm_stream=comm)
 
-        gather_mode = "none" if world == 1 else "%s all_gather (chunked)" % args.backend
+        gather_mode = "none" if world == 1 else "%s all_gather (%d chunk%s)" % (
+            args.backend, len(sb.cb), "s" if len(sb.cb) > 1 else "")
         fused_fg = None
+        probe = None
         if world > 1 and args.gather in ("auto", "fused"):
+            # the fused epilogue runs here only after it has passed the same check in an
+            # isolated process group under a hard timeout (a stall or a fault there cannot
+            # take this run down with it)
+            probe = isolated_fused_probe(args, world, rank, dist)
+            if not probe["ok"]:
+                gather_mode += " (fused epilogue not used: %s)" % probe["why"]
+        if world > 1 and args.gather in ("auto", "fused") and probe["ok"]:
             # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
             # every rank must have built it before any rank runs it, and it is validated
             # bitwise against the NCCL gather before it is used
@@ -727,6 +869,9 @@ def main():
             "cuda_graph": bool(use_graph)}
     if args.workload in ("cfg4", "cfg5"):
         line["config"]["gather"] = gather_mode
+        line["config"]["gather_chunks"] = len(sb.cb)
+        if probe is not None:
+            line["config"]["fused_probe"] = probe
         if world > 1:
             # the gathered result after the timed steps must equal a single-GPU batch of
             # all points, bit for bit (checked on rank 0, outside the timed region)

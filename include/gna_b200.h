@@ -178,7 +178,8 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
  *                              writes every participating GPU's copy (all-gather);
  *   | GNA_PREC_MIXED           the mixed-precision tier below (with flags = GNA_PREC_MIXED
  *                              alone the outputs are local device memory, validated as
- *                              in gna_oscprob_batch).
+ *                              in gna_oscprob_batch);
+ *   | GNA_WS_TABLES_VALID      reuse the node tables already in the workspace (below).
  * The caller synchronises the ranks after the call (e.g. a symmetric-memory or
  * NCCL barrier on the stream) before reading the gathered result.  Inputs and the
  * workspace must be this GPU's memory; output pointers are not type-checked.
@@ -197,6 +198,16 @@ int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const doub
  * tolerance; measured <= 8.2e-7 on cfg4/cfg5) — not the
  * 1e-12 / 1e-11 of the default path.                                            */
 #define GNA_PREC_MIXED 4u
+/* GNA_WS_TABLES_VALID: the per-node tables at the front of d_workspace (1/E and h*w of
+ * every GL node, 2 * align16(order * nbins * 8) bytes; their offset does not depend on
+ * npoints) were built by an earlier gna_oscprob_batch / _ex call on this workspace with
+ * the same edge values, nbins and order, and that call is complete in stream order.
+ * The call then forms only the per-point coefficients (a2) before the main pass, instead
+ * of re-deriving 1/E for every node ((a1): the energy grid is set up once).
+ * For callers that split one batch over several calls (chunked gathers, fit loops).
+ * Outputs are bitwise identical to a call without the flag.  Validation is unchanged;
+ * a workspace that does not hold such tables gives unspecified results (never a fault). */
+#define GNA_WS_TABLES_VALID 8u
 
 int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const double* omega,
                          int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,

@@ -27,7 +27,7 @@ __all__ = [
     "release", "launch_count", "abi_version", "EXPORTS", "GNA_MAX_ORDER", "GNA_MAX_NBASE",
     "oscprob_scan", "oscprob_scan_workspace_size", "oscprob_eval_ab", "oscprob_batch_ex",
     "gl_integrate_ab", "fit_pattern_search", "fit_workspace_size",
-    "GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED",
+    "GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED", "GNA_WS_TABLES_VALID",
 ]
 
 GNA_OK, GNA_EINVAL, GNA_ECUDA, GNA_ENODEV, GNA_ENOMEM = 0, -1, -2, -3, -4
@@ -49,6 +49,7 @@ EXPORTS = (
 GNA_OUT_PEER = 1
 GNA_OUT_MULTICAST = 2
 GNA_PREC_MIXED = 4
+GNA_WS_TABLES_VALID = 8
 
 
 class GnaError(RuntimeError):
@@ -205,6 +206,30 @@ def _small(a, name) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64).ravel())
 
 
+def _baselines(L_km, omega):
+    """Host arrays L_km[nbase], omega[nbase] of equal length (the C ABI reads nbase of each)."""
+    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    if Lh.size != om.size:
+        raise ValueError("L_km and omega must have the same length (%d vs %d)"
+                         % (Lh.size, om.size))
+    return Lh, om
+
+
+def _scratch(nbytes: int, dev, stream, align: int = 8):
+    """Caller-side workspace for one call.  It is allocated on torch's current stream; when the
+    call is enqueued on another `stream`, the block is recorded on that stream so the caching
+    allocator cannot hand it to other work before the kernels that use it have finished."""
+    import torch
+    extra = align // 8
+    ws = torch.empty(max((nbytes + 7) // 8, 2) + extra, dtype=torch.float64, device=dev)
+    if stream is not None:
+        if not isinstance(stream, torch.cuda.Stream):
+            raise TypeError("pass workspace= explicitly when stream is a raw handle")
+        ws.record_stream(stream)
+    off = (-ws.data_ptr()) % align // 8
+    return ws[off:]
+
+
 # ---------------------------------------------------------------- device entry points
 def _prec_flags(precision: str) -> int:
     if precision not in ("fp64", "mixed"):
@@ -289,7 +314,8 @@ def oscprob_batch_workspace_size(npoints: int, nbase: int, nbins: int, order: in
 
 
 def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spectra=True,
-                  chi2=None, workspace=None, stream=None, precision: str = "fp64"):
+                  chi2=None, workspace=None, stream=None, precision: str = "fp64",
+                  tables_valid: bool = False):
     """Batched spectra and chi^2 (gna_oscprob_batch).
 
     points: dict of CUDA float64 tensors theta12, theta13, dm2_21, dm2_31 [P].
@@ -297,6 +323,8 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
     chi2: computed when `data` is given (a [P] tensor may be passed to fill).
     precision: "fp64" (gna_oscprob_batch, the 1e-11 tier) or "mixed" (gna_oscprob_batch_ex
     with GNA_PREC_MIXED: fp64 phases, fp32 polynomial and term sums; 1e-5 tier).
+    tables_valid: the caller's `workspace` already holds the node tables of an earlier call
+    with the same edges and order (GNA_WS_TABLES_VALID; bitwise the same result).
     Returns (spectra or None, chi2 or None).
     """
     _prec_flags(precision)
@@ -311,21 +339,20 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
         spectra = None
     if data is not None and chi2 is None:
         chi2 = torch.empty(P, dtype=torch.float64, device=dev)
-    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
-    if workspace is None:
-        ws_bytes = oscprob_batch_workspace_size(P, Lh.size, nbins, order)
-        workspace = torch.empty(max(ws_bytes // 8, 2), dtype=torch.float64, device=dev)
+    Lh, om = _baselines(L_km, omega)
     b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
-    if Lh.size != om.size:
-        raise ValueError("L_km and omega must have the same length")
+    if workspace is None:
+        workspace = _scratch(oscprob_batch_workspace_size(P, Lh.size, nbins, order), dev, stream)
     args = (ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"),
             nbins, int(order), _dev(spectra, "spectra", P * nbins) if spectra is not None else None,
             _dev(data, "data", nbins) if data is not None else None,
             _dev(chi2, "chi2", P) if chi2 is not None else None,
             _dev(workspace, "workspace"), workspace.numel() * 8)
-    if precision == "mixed":
-        _check(L.gna_oscprob_batch_ex(*args, GNA_PREC_MIXED, _stream(stream)),
-               "gna_oscprob_batch_ex")
+    flags = _prec_flags(precision) | (GNA_WS_TABLES_VALID if tables_valid else 0)
+    if tables_valid and workspace is None:
+        raise ValueError("tables_valid needs the workspace that holds the tables")
+    if flags:
+        _check(L.gna_oscprob_batch_ex(*args, flags, _stream(stream)), "gna_oscprob_batch_ex")
     else:
         _check(L.gna_oscprob_batch(*args, _stream(stream)), "gna_oscprob_batch")
     return spectra, chi2
@@ -352,17 +379,12 @@ def oscprob_scan(grid: dict, L_km, omega, edges, order: int, data=None, spectra=
         spectra = None
     if data is not None and chi2 is None:
         chi2 = torch.empty((nmass, nmix), dtype=torch.float64, device=dev)
-    if workspace is None:
-        wb = oscprob_scan_workspace_size(nmix, nmass, nbins)
-        workspace = torch.empty(max(wb // 8, 4) + 4, dtype=torch.float64, device=dev)
-        off = (-workspace.data_ptr()) % 32 // 8  # 32-byte alignment
-        workspace = workspace[off:]
+    Lh, om = _baselines(L_km, omega)
+    if workspace is None:  # 32-byte aligned
+        workspace = _scratch(oscprob_scan_workspace_size(nmix, nmass, nbins), dev, stream, 32)
     g = _CScan(_dev(grid["theta12"], "theta12", nmix), _dev(grid["theta13"], "theta13", nmix),
                nmix, _dev(grid["dm2_21"], "dm2_21", nmass), _dev(grid["dm2_31"], "dm2_31", nmass),
                nmass)
-    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
-    if Lh.size != om.size:
-        raise ValueError("L_km and omega must have the same length")
     _check(L.gna_oscprob_scan(
         ctypes.byref(g), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins,
         int(order),
@@ -381,10 +403,10 @@ def oscprob_batch_ex(points: dict, L_km, omega, edges, order: int, spectra_ptr: 
     L = load()
     P = points["theta12"].numel()
     nbins = edges.numel() - 1
-    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    Lh, om = _baselines(L_km, omega)
     if workspace is None:
-        wb = oscprob_batch_workspace_size(P, Lh.size, nbins, order)
-        workspace = torch.empty(max(wb // 8, 2), dtype=torch.float64, device=edges.device)
+        workspace = _scratch(oscprob_batch_workspace_size(P, Lh.size, nbins, order),
+                             edges.device, stream)
     b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
     _check(L.gna_oscprob_batch_ex(
         ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins,
@@ -404,12 +426,11 @@ def fit_pattern_search(state, L_km, omega, edges, order: int, data, niter: int, 
     import torch
     L = load()
     nbins = edges.numel() - 1
-    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    Lh, om = _baselines(L_km, omega)
     if hist is None and niter > 0:
         hist = torch.empty(niter, dtype=torch.float64, device=edges.device)
     if workspace is None:
-        wb = fit_workspace_size(Lh.size, nbins, order)
-        workspace = torch.empty(max(wb // 8, 2), dtype=torch.float64, device=edges.device)
+        workspace = _scratch(fit_workspace_size(Lh.size, nbins, order), edges.device, stream)
     _check(L.gna_fit_pattern_search(
         Lh.ctypes.data, om.ctypes.data, Lh.size, _dev(edges, "edges"), nbins, int(order),
         _dev(data, "data", nbins), _dev(state, "state", 8), int(niter),
@@ -455,8 +476,8 @@ def oscprob_batch_host(points: dict, L_km, omega, edges: np.ndarray, order: int,
                        chunk_points: int = 0, stream=None):
     """Batch over HOST arrays (end-to-end path); returns (spectra, chi2) numpy arrays."""
     L = load()
-    pts = {k: _host(points[k], k) for k in ("theta12", "theta13", "dm2_21", "dm2_31")}
-    P = pts["theta12"].size
+    P = _host(points["theta12"], "theta12").size
+    pts = {k: _host(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")}
     edges = _host(edges, "edges")
     nbins = edges.size - 1
     if spectra is True:
@@ -472,7 +493,7 @@ def oscprob_batch_host(points: dict, L_km, omega, edges: np.ndarray, order: int,
     if chi2 is not None:
         _host(chi2, "chi2", P, writable=True)
     b = _CBatch(*(pts[k].ctypes.data for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
-    Lh, om = _small(L_km, "L_km"), _small(omega, "omega")
+    Lh, om = _baselines(L_km, omega)
     _check(L.gna_oscprob_batch_host(
         ctypes.byref(b), Lh.ctypes.data, om.ctypes.data, Lh.size, edges.ctypes.data, nbins,
         int(order), spectra.ctypes.data if spectra is not None else None,

@@ -225,12 +225,30 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, si
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// single-point kernels (GL, elementwise): PDL when GNA_PDL_SINGLE (they wait before their
+// first input load, gna_common.cuh), else a plain stream-ordered launch
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl_single(void (*kern)(KArgs...), unsigned grid, unsigned block,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (GNA_PDL && GNA_PDL_SINGLE) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // launch of the batch kernels on already-validated device arguments
 template <int kOut, bool kMixed>
 int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double* omega,
                    int32_t nbase, const double* edges, int64_t nbins, int32_t order,
                    double* spectra, const double* data, double* chi2, void* workspace,
-                   cudaStream_t s) {
+                   cudaStream_t s, const double* tables) {
   BatchSetupArgs a;
   std::memset(&a, 0, sizeof(a));
   double om = 0.0;
@@ -244,7 +262,14 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   a.order = order;
   a.nbins = nbins;
   a.npoints = pts->npoints;
-  const BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
+  BatchWs w = batch_ws_carve(workspace, pts->npoints, nbase, nbins, order, chi2 != nullptr);
+  // tables: node tables built earlier (invE at tables, hw right after, batch_ws_carve's
+  // layout); the setup kernel then only forms the per-point coefficients
+  a.tables = tables == nullptr;
+  if (tables) {
+    w.invE = const_cast<double*>(tables);
+    w.hw = (double*)((char*)w.invE + align16((size_t)order * nbins * sizeof(double)));
+  }
   const int64_t bpp = blocks_per_point(nbins);
   // points per warp: enough sin^2 work per lane to amortise the per-point overhead
   // (>= GNA_BATCH_PPW_WORK_BIG; >= GNA_BATCH_PPW_WORK for the small-nbase points-inner
@@ -260,7 +285,7 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   while (ppw > 1 && ((pts->npoints + ppw - 1) / ppw) * bpp < min_blocks) ppw >>= 1;
   const int64_t ngroups = (pts->npoints + ppw - 1) / ppw;
   const int64_t nblocks = ngroups * bpp;
-  const int64_t nsetup = pts->npoints * nbase + (int64_t)order * nbins;
+  const int64_t nsetup = pts->npoints * nbase + (a.tables ? (int64_t)order * nbins : 0);
   if (nblocks > 0x7fffffffLL || (nsetup + 255) / 256 > 0x7fffffffLL) return GNA_EINVAL;
 
   k_batch_setup<<<(unsigned)((nsetup + 255) / 256), 256, 0, s>>>(
@@ -355,12 +380,35 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
   return GNA_OK;
 }
 
+// tables_only: k_batch_setup building just the node tables (invE, hw) at `tables`
+int launch_batch_tables(const double* edges, int64_t nbins, int32_t order, double* tables,
+                        cudaStream_t s) {
+  BatchSetupArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.order = order;
+  a.nbins = nbins;
+  a.npoints = 0;
+  a.tables = 1;
+  BatchWs w;
+  std::memset(&w, 0, sizeof(w));
+  w.invE = tables;
+  w.hw = (double*)((char*)tables + align16((size_t)order * nbins * sizeof(double)));
+  const int64_t n = (int64_t)order * nbins;
+  if ((n + 255) / 256 > 0x7fffffffLL) return GNA_EINVAL;
+  k_batch_setup<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, nullptr, nullptr, nullptr,
+                                                             nullptr, edges, w);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+
 int launch_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
                  int32_t nbase, const double* edges, int64_t nbins, int32_t order,
                  double* spectra, const double* data, double* chi2, void* workspace,
-                 cudaStream_t s, int out_mode = kOutLocal, bool mixed = false) {
+                 cudaStream_t s, int out_mode = kOutLocal, bool mixed = false,
+                 const double* tables = nullptr) {
 #define GNA_LB(M, X) launch_batch_k<M, X>(pts, L_km, omega, nbase, edges, nbins, order, spectra, \
-                                          data, chi2, workspace, s)
+                                          data, chi2, workspace, s, tables)
   if (mixed) {
     if (out_mode == kOutMulticast) return GNA_LB(kOutMulticast, true);
     if (out_mode == kOutPeer) return GNA_LB(kOutPeer, true);
@@ -409,19 +457,38 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
 template <class Coef>
 int launch_gl(const Coef& c, const double* edges, int64_t nbins, int order, double* bins,
               cudaStream_t s) {
-  if (nbins >= gl_tb_min_bins<Coef>()) {
+  constexpr bool kPee = std::is_same<Coef, PeeCoef>::value;
+  if (kPee && GNA_GL_SPLIT && order >= 2 && nbins <= GNA_GL_SPLIT_MAX_BINS) {
+    // node halves in two warps (k_gl.cuh), the same bits as thread per bin
+    const int64_t grid = (nbins + 32 * kGLSplitBW - 1) / (32 * kGLSplitBW);
+    const gl_kernel_t<Coef> kern =
+        gl_split_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+    cudaError_t e = launch_pdl_single(kern, (unsigned)grid, kGLSplitThreads, s, c, edges, nbins,
+                                      bins);
+    if (e != cudaSuccess) return cuda_fail(e);
+  } else if (nbins >= gl_tb_min_bins<Coef>()) {
     // thread per bin, GL table as uniform constant-bank operands (k_gl.cuh)
     const int64_t grid = (nbins + kGLTbThreads - 1) / kGLTbThreads;
     if (grid > 0x7fffffffLL) return GNA_EINVAL;
     const gl_kernel_t<Coef> kern =
         gl_tb_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
-    kern<<<(unsigned)grid, kGLTbThreads, 0, s>>>(c, edges, nbins, bins);
+    cudaError_t e = launch_pdl_single(kern, (unsigned)grid, kGLTbThreads, s, c, edges, nbins,
+                                      bins);
+    if (e != cudaSuccess) return cuda_fail(e);
   } else {
-    const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
-    if (grid > 0x7fffffffLL) return GNA_EINVAL;
-    const gl_kernel_t<Coef> kern =
-        gl_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
-    kern<<<(unsigned)grid, kGLLaneThreads, 0, s>>>(c, edges, nbins, bins);
+    // lane pairs (mixed tier and general channel only: not instantiated for P_ee fp64,
+    // whose gl_tb_min_bins is 1)
+    if constexpr (gl_tb_min_bins<Coef>() > 1) {
+      const int64_t grid = (2 * nbins + kGLLaneThreads - 1) / kGLLaneThreads;
+      if (grid > 0x7fffffffLL) return GNA_EINVAL;
+      const gl_kernel_t<Coef> kern =
+          gl_kernel_for<Coef>(order, std::make_integer_sequence<int, GNA_MAX_ORDER>{});
+      cudaError_t e = launch_pdl_single(kern, (unsigned)grid, kGLLaneThreads, s, c, edges,
+                                        nbins, bins);
+      if (e != cudaSuccess) return cuda_fail(e);
+    } else {
+      return GNA_EINVAL;  // unreachable: nbins >= 1 was validated
+    }
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -436,13 +503,19 @@ int launch_eval(const Coef& c, const double* E, int64_t n, double* P, cudaStream
     // persistent TMA-fed stream: GNA_EVAL_MINB blocks per SM (4 x 8 KiB smem ring each)
     const int64_t ntiles = n / kEvalTile;
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * GNA_EVAL_MINB);
-    k_oscprob_eval_tma<Coef><<<grid, kEvalTmaThreads, 0, s>>>(c, E, P, n);
+    cudaError_t e = launch_pdl_single(k_oscprob_eval_tma<Coef>, (unsigned)grid, kEvalTmaThreads,
+                                      s, c, E, P, n);
+    if (e != cudaSuccess) return cuda_fail(e);
   } else if (vec) {
     const int grid = grid_for((n + 1) / 2, kEvalThreads, maxb);
-    k_oscprob_eval<true, Coef><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+    cudaError_t e = launch_pdl_single(k_oscprob_eval<true, Coef>, (unsigned)grid, kEvalThreads,
+                                      s, c, E, P, n);
+    if (e != cudaSuccess) return cuda_fail(e);
   } else {
     const int grid = grid_for(n, kEvalThreads, maxb);
-    k_oscprob_eval<false, Coef><<<grid, kEvalThreads, 0, s>>>(c, E, P, n);
+    cudaError_t e = launch_pdl_single(k_oscprob_eval<false, Coef>, (unsigned)grid, kEvalThreads,
+                                      s, c, E, P, n);
+    if (e != cudaSuccess) return cuda_fail(e);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
@@ -624,11 +697,30 @@ size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t 
   return batch_ws_bytes(npoints, nbase, nbins, order, true);
 }
 
+// The batch workspace must not alias any input or local output: k_batch_setup writes the
+// coefficient rows and node tables into it before the main kernel reads the inputs.  Remote
+// outputs (peer / multicast windows) are other GPUs' memory and pass nullptr here.
+static bool batch_ws_overlaps(const gna_param_batch* pts, const double* d_edges, int64_t nbins,
+                              int32_t order, int32_t nbase, const double* d_data,
+                              const double* d_spectra, const double* d_chi2, bool want_chi2,
+                              const void* d_workspace) {
+  const size_t W = batch_ws_bytes(pts->npoints, nbase, nbins, order, want_chi2);
+  const size_t P8 = (size_t)pts->npoints * 8;
+  const void* ins[8] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31,
+                        d_edges,      d_spectra,    d_data,     d_chi2};
+  const size_t ln[8] = {P8, P8, P8, P8, (size_t)(nbins + 1) * 8,
+                        (size_t)pts->npoints * (size_t)nbins * 8, (size_t)nbins * 8, P8};
+  for (int i = 0; i < 8; ++i)
+    if (ins[i] && overlap(d_workspace, W, ins[i], ln[i])) return true;
+  return false;
+}
+
 // gna_oscprob_batch and the local-output case of gna_oscprob_batch_ex (fp64 or mixed tier)
 static int batch_local(const gna_param_batch* pts, const double* L_km, const double* omega,
                        int32_t nbase, const double* d_edges, int64_t nbins, int32_t order,
                        double* d_spectra, const double* d_data, double* d_chi2,
-                       void* d_workspace, size_t workspace_bytes, void* stream, bool mixed) {
+                       void* d_workspace, size_t workspace_bytes, void* stream, bool mixed,
+                       bool tables_valid = false) {
   int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
                           d_chi2);
   if (rc) return rc;
@@ -636,23 +728,17 @@ static int batch_local(const gna_param_batch* pts, const double* L_km, const dou
       workspace_bytes < batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr) ||
       ((uintptr_t)d_workspace & 15))
     return GNA_EINVAL;
-  {
-    const size_t W = batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr);
-    const size_t P8 = (size_t)pts->npoints * 8;
-    const void* ins[8] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31,
-                          d_edges,      d_spectra,    d_data,     d_chi2};
-    const size_t ln[8] = {P8, P8, P8, P8, (size_t)(nbins + 1) * 8,
-                          (size_t)pts->npoints * (size_t)nbins * 8, (size_t)nbins * 8, P8};
-    for (int i = 0; i < 8; ++i)
-      if (ins[i] && overlap(d_workspace, W, ins[i], ln[i])) return GNA_EINVAL;
-  }
+  if (batch_ws_overlaps(pts, d_edges, nbins, order, nbase, d_data, d_spectra, d_chi2,
+                        d_chi2 != nullptr, d_workspace))
+    return GNA_EINVAL;
   if ((rc = check_device())) return rc;
   const void* ptrs[9] = {pts->theta12, pts->theta13, pts->dm2_21, pts->dm2_31, d_edges,
                          d_spectra,    d_data,       d_chi2,      d_workspace};
   for (const void* q : ptrs)
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
-                      d_workspace, (cudaStream_t)stream, kOutLocal, mixed);
+                      d_workspace, (cudaStream_t)stream, kOutLocal, mixed,
+                      tables_valid ? (const double*)d_workspace : nullptr);
 }
 
 int gna_oscprob_batch(const gna_param_batch* pts, const double* L_km, const double* omega,
@@ -733,10 +819,12 @@ int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbas
   if (niter > 0) {
     k_fit_candidates<<<1, 128, 0, s>>>(d_state, cand);
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    // the node tables depend only on the edges and the order: built once per fit
+    if ((rc = launch_batch_tables(d_edges, nbins, order, (double*)bws, s))) return rc;
   }
   for (int it = 0; it < niter; ++it) {
     if ((rc = launch_batch(&pts, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data,
-                           chi2, bws, s)))
+                           chi2, bws, s, kOutLocal, false, (const double*)bws)))
       return rc;
     k_fit_update<<<1, 128, 0, s>>>(d_state, cand, chi2, d_hist, it, it + 1 < niter);
     g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -751,19 +839,24 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
                          double* d_spectra, const double* d_data, double* d_chi2,
                          void* d_workspace, size_t workspace_bytes, uint32_t flags,
                          void* stream) {
-  const uint32_t known = GNA_OUT_PEER | GNA_OUT_MULTICAST | GNA_PREC_MIXED;
+  const uint32_t known = GNA_OUT_PEER | GNA_OUT_MULTICAST | GNA_PREC_MIXED | GNA_WS_TABLES_VALID;
   if ((flags & ~known) || ((flags & GNA_OUT_PEER) && (flags & GNA_OUT_MULTICAST)))
     return GNA_EINVAL;
   const bool mixed = (flags & GNA_PREC_MIXED) != 0;
+  const bool tables_valid = (flags & GNA_WS_TABLES_VALID) != 0;
   if ((flags & (GNA_OUT_PEER | GNA_OUT_MULTICAST)) == 0)
     return batch_local(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
-                       d_workspace, workspace_bytes, stream, mixed);
+                       d_workspace, workspace_bytes, stream, mixed, tables_valid);
   int rc = validate_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data,
                           d_chi2);
   if (rc) return rc;
   if (!d_workspace ||
       workspace_bytes < batch_ws_bytes(pts->npoints, nbase, nbins, order, d_chi2 != nullptr) ||
       ((uintptr_t)d_workspace & 15))
+    return GNA_EINVAL;
+  // remote outputs are excluded from the overlap check (they are not this GPU's memory)
+  if (batch_ws_overlaps(pts, d_edges, nbins, order, nbase, d_data, nullptr, nullptr,
+                        d_chi2 != nullptr, d_workspace))
     return GNA_EINVAL;
   if ((rc = check_device())) return rc;
   // inputs and workspace must be this GPU's memory; the outputs are remote windows
@@ -773,7 +866,8 @@ int gna_oscprob_batch_ex(const gna_param_batch* pts, const double* L_km, const d
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   return launch_batch(pts, L_km, omega, nbase, d_edges, nbins, order, d_spectra, d_data, d_chi2,
                       d_workspace, (cudaStream_t)stream,
-                      (flags & GNA_OUT_MULTICAST) ? kOutMulticast : kOutPeer, mixed);
+                      (flags & GNA_OUT_MULTICAST) ? kOutMulticast : kOutPeer, mixed,
+                      tables_valid ? (const double*)d_workspace : nullptr);
 }
 
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
@@ -848,9 +942,12 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   const size_t need = (n_ws + n_par + n_spec + n_chi) * 8;
   for (int i = 0; i < 2; ++i)
     if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  // shared by the chunks: node tables (built once per call, 16-aligned, first), edges, data
+  const size_t tb = batch_tables_bytes(nbins, order);
   const size_t n_shared = (size_t)(nbins + 1) + (h_data ? (size_t)nbins : 0);
-  if ((rc = ensure(&S->shared, &S->shared_cap, n_shared * 8))) return rc;
-  double* d_edges = (double*)S->shared;
+  if ((rc = ensure(&S->shared, &S->shared_cap, tb + n_shared * 8))) return rc;
+  double* d_tables = (double*)S->shared;
+  double* d_edges = (double*)((char*)S->shared + tb);
   double* d_data = h_data ? d_edges + (nbins + 1) : nullptr;
 
   cudaError_t e;
@@ -862,6 +959,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   if (d_data &&
       (e = cudaMemcpyAsync(d_data, h_data, (size_t)nbins * 8, cudaMemcpyHostToDevice, s0)))
     return cuda_fail(e);
+  if ((rc = launch_batch_tables(d_edges, nbins, order, d_tables, s0))) return rc;
   if ((e = cudaEventRecord(S->ev_in, s0)) != cudaSuccess) return cuda_fail(e);
   if ((e = cudaStreamWaitEvent(S->st[1], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
 
@@ -884,7 +982,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
     gna_param_batch dp = {dpar, dpar + chunk_points, dpar + 2 * chunk_points,
                           dpar + 3 * chunk_points, m};
     if ((rc = launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data, dchi,
-                           dws, s)))
+                           dws, s, kOutLocal, false, d_tables)))
       return rc;
     if (h_spectra && (e = cudaMemcpyAsync(h_spectra + o * nbins, dspec, (size_t)m * nbins * 8,
                                           cudaMemcpyDeviceToHost, s)))

@@ -56,6 +56,31 @@ __host__ __device__ inline void mixing_weights(double s12, double c12, double s1
   *w32 = (s2t13 * s2t13) * (s12 * s12);
 }
 
+// Programmatic dependent launch (sm_90+; GNA_PDL): a kernel launched with the
+// programmatic-stream-serialization attribute may start while its predecessor on the stream
+// finishes; it waits here (griddepcontrol.wait: the predecessor grid has completed and its
+// memory is visible) before it reads anything a predecessor may have written.  The batch main
+// pass and chi2 reduce wait for their setup / main pass; the single-point GL and elementwise
+// kernels (GNA_PDL_SINGLE) wait before their first input load, so only launch latency and
+// block rasterisation overlap the previous call — never a read of its outputs.  Without a
+// programmatic dependency both instructions are no-ops.
+#ifndef GNA_PDL
+#define GNA_PDL 1
+#endif
+#ifndef GNA_PDL_SINGLE
+#define GNA_PDL_SINGLE 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if GNA_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if GNA_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 // ----------------------------------------------------------------------------
 // kernels
 size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }

@@ -13,28 +13,14 @@ struct BatchSetupArgs {
   int order;
   int64_t nbins;
   int64_t npoints;
+  int tables;  // 1: also build the per-node tables invE / hw (0: the caller's are valid)
 };
 
-// Programmatic dependent launch (sm_90+; GNA_PDL): the main pass is launched while the setup
-// kernel still runs and waits for it here; the chi2 reduce likewise waits for the main pass.
-// Without a programmatic dependency both instructions are no-ops.
-#ifndef GNA_PDL
-#define GNA_PDL 1
-#endif
-__device__ __forceinline__ void pdl_wait() {
-#if GNA_PDL
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void pdl_launch_dependents() {
-#if GNA_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
-
 // Workspace layout of the batch path (all offsets 16-byte aligned), see
-// gna_oscprob_batch_workspace_size:  coef [P][nbase][3] double2 (kq, omega_b w_ij),
-// c0 [P], invE [order][nbins], hw [order][nbins], partial [P][wpp][S] (S = 1 except for
+// gna_oscprob_batch_workspace_size:  invE [order][nbins], hw [order][nbins] first (their
+// offsets do not depend on the number of points, so a caller that splits its points over
+// several calls can keep one set of node tables: GNA_WS_TABLES_VALID), then coef
+// [P][nbase][3] double2 (kq, omega_b w_ij), c0 [P], partial [P][wpp][S] (S = 1 except for
 // k_oscprob_batch_pt sub-tiles; sized for S = kPtSubMax).
 struct BatchWs {
   double2* coef;
@@ -44,16 +30,18 @@ struct BatchWs {
   double* partial;
 };
 
-
-
 // chi2 partials per (point, 32-bin tile); the points-across-lanes kernel may split a tile
 // into up to kPtSubMax sub-tiles, each with its own partial (k_oscprob_batch_pt)
 constexpr int kPtSubMax = 4;
 
+size_t batch_tables_bytes(int64_t nbins, int order) {
+  return 2 * align16((size_t)order * nbins * sizeof(double));
+}
+
 size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
-  size_t b = align16((size_t)P * nbase * 3 * sizeof(double2));
+  size_t b = batch_tables_bytes(nbins, order);
+  b += align16((size_t)P * nbase * 3 * sizeof(double2));
   b += align16((size_t)P * sizeof(double));
-  b += 2 * align16((size_t)order * nbins * sizeof(double));
   if (chi2) b += align16((size_t)P * warps_per_point(nbins) * kPtSubMax * sizeof(double));
   return b;
 }
@@ -61,14 +49,14 @@ size_t batch_ws_bytes(int64_t P, int nbase, int64_t nbins, int order, bool chi2)
 BatchWs batch_ws_carve(void* base, int64_t P, int nbase, int64_t nbins, int order, bool chi2) {
   char* c = (char*)base;
   BatchWs w;
-  w.coef = (double2*)c;
-  c += align16((size_t)P * nbase * 3 * sizeof(double2));
-  w.c0 = (double*)c;
-  c += align16((size_t)P * sizeof(double));
   w.invE = (double*)c;
   c += align16((size_t)order * nbins * sizeof(double));
   w.hw = (double*)c;
   c += align16((size_t)order * nbins * sizeof(double));
+  w.coef = (double2*)c;
+  c += align16((size_t)P * nbase * 3 * sizeof(double2));
+  w.c0 = (double*)c;
+  c += align16((size_t)P * sizeof(double));
   w.partial = chi2 ? (double*)c : nullptr;
   return w;
 }
@@ -84,7 +72,7 @@ __global__ void __launch_bounds__(256) k_batch_setup(BatchSetupArgs a,
   pdl_launch_dependents();  // the main pass may be scheduled now; it waits in pdl_wait()
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = a.npoints * a.nbase;
-  const int64_t n2 = (int64_t)a.order * a.nbins;
+  const int64_t n2 = a.tables ? (int64_t)a.order * a.nbins : 0;
   if (t < n1) {
     const int64_t p = t / a.nbase;
     const int b = (int)(t - p * a.nbase);

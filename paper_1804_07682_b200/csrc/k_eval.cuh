@@ -12,6 +12,8 @@ __global__ void __launch_bounds__(kEvalThreads) k_oscprob_eval(Coef c,
                                                                double* __restrict__ P, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();
   if (kVec) {
     const int64_t n2 = n >> 1;
     const double2* __restrict__ E2 = reinterpret_cast<const double2*>(E);
@@ -66,6 +68,8 @@ __global__ void __launch_bounds__(kEvalTmaThreads, GNA_EVAL_MINB) k_oscprob_eval
     for (int st = 0; st < kEvalStages; ++st) gna::mbar_init(&s_full[st], 1);
     gna::fence_mbar_init();
   }
+  pdl_launch_dependents();
+  pdl_wait();  // before the first read of E (a predecessor may have written it)
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int st = 0; st < kEvalStages && st < mine; ++st) {

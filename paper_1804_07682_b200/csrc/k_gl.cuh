@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Co
   const int half = (int)(t & 1);
   const bool act = k < nbins;
   const int64_t kk = act ? k : nbins - 1;
+  pdl_launch_dependents();
+  pdl_wait();
   const double e0 = edges[kk], e1 = edges[kk + 1];
   const double ctr = 0.5 * (e0 + e1);
   const double h = 0.5 * (e1 - e0);
@@ -66,9 +68,11 @@ __global__ void __launch_bounds__(kGLLaneThreads, GNA_GL_MINB) k_gl_integrate(Co
 #endif
 // nbins from which the thread-per-bin kernel is used, per coefficient type (below: lane
 // pairs).  Back-to-back launch times, tools/gl_b2b.py (profiles/r01_gl_b2b.jsonl): P_ee fp64
-// is faster (or equal) with thread per bin at every size from 1 bin up (cfg1 1.79 -> 1.54 us,
-// cfg2 4.76 -> 4.53 us); the mixed tier and the general channel are faster with lane pairs
-// up to ~10^5 bins and with thread per bin at 10^6.
+// is faster (or equal) with thread per bin than with lane pairs at every size from 1 bin up
+// (cfg1 1.79 -> 1.54 us, cfg2 4.76 -> 4.53 us), so the lane-pair kernel is not even built for
+// it (launch_gl); small P_ee grids take the warp-split kernel below instead.  The mixed tier
+// and the general channel are faster with lane pairs up to ~10^5 bins and with thread per bin
+// at 10^6.
 #ifndef GNA_GL_TB_MIN_BINS
 #define GNA_GL_TB_MIN_BINS 1
 #endif
@@ -99,7 +103,9 @@ __global__ void __launch_bounds__(kGLTbThreads, GNA_GL_TB_MINB) k_gl_integrate_t
   constexpr int G = gl_group(kOrder);
   constexpr int off = GNA_GL_OFF(kOrder);
   const int64_t k = (int64_t)blockIdx.x * kGLTbThreads + threadIdx.x;
+  pdl_launch_dependents();
   if (k >= nbins) return;
+  pdl_wait();
   const double e0 = edges[k], e1 = edges[k + 1];
   const double ctr = 0.5 * (e0 + e1);
   const double h = 0.5 * (e1 - e0);
@@ -125,8 +131,84 @@ __global__ void __launch_bounds__(kGLTbThreads, GNA_GL_TB_MINB) k_gl_integrate_t
   bins[k] = h * (s0 + s1);
 }
 
+// Sum over the nodes [kLo, kHi) of one bin, ascending, w_i P(c + h t_i) accumulated with
+// FMAs, the nodes taken G at a time (independent reciprocal + sin^2 chains).  A node's P does
+// not depend on the group it is evaluated in, so any grouping gives the same bits.
+template <int kOrder, int kLo, int kHi, class Coef>
+__device__ __forceinline__ double gl_nodes_sum(const Coef& c, double ctr, double h) {
+  constexpr int off = GNA_GL_OFF(kOrder);
+  constexpr int G = gl_group(kHi - kLo > 0 ? kHi - kLo : 1);
+  double s = 0.0;
+#pragma unroll
+  for (int i0 = kLo; i0 < kHi; i0 += G) {
+    const int n = kHi - i0 < G ? kHi - i0 : G;
+    double iE[G], pv[G];
+#pragma unroll
+    for (int i = 0; i < G; ++i) iE[i] = gna::rcp(fma(h, c_gl_t[off + (i < n ? i0 + i : i0)], ctr));
+    gna::prob_inv_n<G>(c, iE, pv);
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+      if (i < n) s = fma(c_gl_w[off + i0 + i], pv[i], s);
+  }
+  return s;
+}
+
+// Grids smaller than a few waves (cfg2: 10^5 bins = 0.75 waves of the thread-per-bin kernel,
+// 25 % of the warps active): the two node halves of a bin run in two different warps of one
+// block — warp w < BW takes nodes [0, H) of 32 bins, warp BW + w nodes [H, order) of the same
+// bins — and meet in shared memory: bins[k] = h (s0 + s1), the thread-per-bin kernel's
+// arithmetic to the bit.  Twice the threads, half the dependent chain per thread, and node
+// indices stay warp-uniform (constant-bank operands).
+#ifndef GNA_GL_SPLIT
+#define GNA_GL_SPLIT 1
+#endif
+#ifndef GNA_GL_SPLIT_BW
+#define GNA_GL_SPLIT_BW 2
+#endif
+#ifndef GNA_GL_SPLIT_MINB
+#define GNA_GL_SPLIT_MINB 4
+#endif
+// P_ee fp64 takes the split kernel for 2 <= order and nbins <= this (above: thread per bin)
+#ifndef GNA_GL_SPLIT_MAX_BINS
+#define GNA_GL_SPLIT_MAX_BINS 262144
+#endif
+constexpr int kGLSplitBW = GNA_GL_SPLIT_BW;
+constexpr int kGLSplitThreads = 64 * kGLSplitBW;
+
+template <int kOrder, class Coef>
+__global__ void __launch_bounds__(kGLSplitThreads, GNA_GL_SPLIT_MINB) k_gl_integrate_split(
+    Coef c, const double* __restrict__ edges, int64_t nbins, double* __restrict__ bins) {
+  constexpr int H = (kOrder + 1) / 2;
+  __shared__ double s_hi[32 * kGLSplitBW];
+  const int warp = threadIdx.x >> 5;
+  const int upper = warp >= kGLSplitBW;  // warp-uniform
+  const int slot = (warp - upper * kGLSplitBW) * 32 + (threadIdx.x & 31);
+  const int64_t k = (int64_t)blockIdx.x * (32 * kGLSplitBW) + slot;
+  const int64_t kk = k < nbins ? k : nbins - 1;
+  pdl_launch_dependents();
+  pdl_wait();
+  const double e0 = edges[kk], e1 = edges[kk + 1];
+  const double ctr = 0.5 * (e0 + e1);
+  const double h = 0.5 * (e1 - e0);
+  double s;
+  if (upper) {
+    s = gl_nodes_sum<kOrder, H, kOrder>(c, ctr, h);
+    s_hi[slot] = s;
+  } else {
+    s = gl_nodes_sum<kOrder, 0, H>(c, ctr, h);
+  }
+  __syncthreads();
+  if (!upper && k < nbins) bins[k] = h * (s + s_hi[slot]);
+}
+
 template <class Coef>
 using gl_kernel_t = void (*)(Coef, const double*, int64_t, double*);
+
+template <class Coef, int... N>
+gl_kernel_t<Coef> gl_split_kernel_for(int order, std::integer_sequence<int, N...>) {
+  static const gl_kernel_t<Coef> t[] = {k_gl_integrate_split<N + 1, Coef>...};
+  return t[order - 1];
+}
 
 template <class Coef, int... N>
 gl_kernel_t<Coef> gl_kernel_for(int order, std::integer_sequence<int, N...>) {

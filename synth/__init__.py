@@ -70,6 +70,18 @@ def points_uniform(g: np.random.Generator, npoints: int, ranges: dict) -> dict:
     return out
 
 
+def invert_ordering(g: np.random.Generator, points: dict, frac: float = 0.25) -> dict:
+    """Copy of `points` with dm2_31 sign-flipped on a random `frac` of them: inverted mass
+    ordering (S:328 signed dm2_31), the DESIGN.md parity-draw recipe.  Works on point lists
+    and on a scan grid's mass axis alike (only the dm2_31 array is touched)."""
+    out = {k: np.array(v, dtype=np.float64, copy=True) for k, v in points.items()}
+    flip = g.random(out["dm2_31"].size) < frac
+    if out["dm2_31"].size >= 2 and not flip.any():
+        flip[-1] = True  # every multi-point draw holds at least one inverted point
+    out["dm2_31"][flip] = -out["dm2_31"][flip]
+    return out
+
+
 def pseudo_data(g: np.random.Generator, edges: np.ndarray, total_weight: float) -> np.ndarray:
     """Positive pseudo-data spectrum: bin width x total baseline weight x U(0.4, 0.9)."""
     width = np.diff(edges)

@@ -154,11 +154,20 @@ def test_batch_einval(lib, case):
     assert _batch(lib, **case) == gna.GNA_EINVAL
     # the mixed tier (NEXT-3) validates exactly like the fp64 batch
     assert _batch(lib, flags=gna.GNA_PREC_MIXED, **case) == gna.GNA_EINVAL
+    assert _batch(lib, flags=gna.GNA_WS_TABLES_VALID, **case) == gna.GNA_EINVAL
     if "ws" not in case and "wsb" not in case:
         assert _batch(lib, host=True, **case) == gna.GNA_EINVAL
 
 
-@pytest.mark.parametrize("flags", [8, 16 | 4, 1 | 2, 1 | 2 | 4, 0xffffffff])
+@pytest.mark.parametrize("flags", [1, 2, 1 | 4, 2 | 4])
+@pytest.mark.parametrize("ws", [0x100000 - 64, 0x500000 - 64, 0x700000 + 8])
+def test_batch_ex_remote_outputs_workspace_overlap_einval(lib, flags, ws):
+    """Peer / multicast outputs: the workspace still must not alias the local inputs
+    (points, edges, data), or k_batch_setup would overwrite them."""
+    assert _batch(lib, flags=flags, ws=ws) == gna.GNA_EINVAL
+
+
+@pytest.mark.parametrize("flags", [16, 16 | 4, 1 | 2, 1 | 2 | 4, 1 | 2 | 8, 0xffffffff])
 def test_batch_ex_bad_flags(lib, flags):
     assert _batch(lib, flags=flags) == gna.GNA_EINVAL
 
@@ -183,7 +192,8 @@ def test_eval_gl_ex_mixed_validates_like_fp64(lib):
 def test_header_constants_match_binding():
     """The Python binding's constants are the header's #defines."""
     src = open(HEADER).read()
-    for name in ("GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED", "GNA_MAX_ORDER",
+    for name in ("GNA_OUT_PEER", "GNA_OUT_MULTICAST", "GNA_PREC_MIXED", "GNA_WS_TABLES_VALID",
+                 "GNA_MAX_ORDER",
                  "GNA_MAX_NBASE", "GNA_OK", "GNA_EINVAL", "GNA_ECUDA", "GNA_ENODEV",
                  "GNA_ENOMEM"):
         m = (re.search(r"#define %s \(?(-?\d+)u?\)?" % name, src) or
@@ -397,3 +407,27 @@ def test_c_abi_example_compiles_and_links(lib, tmp_path):
         pytest.skip("gcc or the CUDA headers are not available")
     exe = compile_c_example(tmp_path / "gl_integrate_c")
     assert os.path.exists(exe)
+
+
+def test_binding_checks_lengths_before_any_call(lib):
+    """The binding rejects mismatched host array lengths before the C ABI (which reads nbase
+    omegas and P values of every point array) could read past a numpy buffer."""
+    import torch
+    P = 4
+    pts = {k: np.full(P, v) for k, v in dict(theta12=0.58, theta13=0.15, dm2_21=7.5e-5,
+                                               dm2_31=2.5e-3).items()}
+    edges = np.linspace(1.0, 10.0, 11)
+    data = np.ones(10)
+    short = dict(pts, theta13=np.full(P - 1, 0.15))
+    with pytest.raises(ValueError):
+        gna.oscprob_batch_host(short, [52.5], [1.0], edges, 5, data=data)
+    with pytest.raises(ValueError):
+        gna.oscprob_batch_host(pts, [52.5, 215.0], [1.0], edges, 5, data=data)
+    with pytest.raises(ValueError):
+        gna.oscprob_batch_host(pts, [52.5], 1.0 * np.ones(3), edges, 5, data=data)
+    tp = {k: torch.tensor(v) for k, v in pts.items()}
+    with pytest.raises(ValueError):
+        gna.oscprob_batch_ex(tp, [52.5, 215.0], [1.0], torch.tensor(edges), 5, None, None, 0)
+    with pytest.raises(ValueError):
+        gna.fit_pattern_search(torch.zeros(8, dtype=torch.float64), [52.5, 215.0], [1.0],
+                               torch.tensor(edges), 5, torch.tensor(data), 1)

@@ -140,3 +140,53 @@ def test_fused_gather_window_arithmetic():
         base_c = (95_000 if mc else 40_000) + 16
         assert sp == base_s + fg.lo * 7 * 8 and x2 == base_c + fg.lo * 8
         assert flags == (2 if mc else 1)
+
+
+def _probe_worker(rank, world, port, timeout, out_q):
+    """Both ranks of a gloo job run bench.isolated_fused_probe: rank 0 starts the isolated
+    N-rank check, the other ranks wait on the store; all must get the same verdict."""
+    import sys
+    from types import SimpleNamespace
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        args = SimpleNamespace(workload="cfg5", precision="fp64", probe_timeout=timeout)
+        out_q.put((rank, bench.isolated_fused_probe(args, world, rank, dist)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("timeout", [0.2, 240.0])
+def test_isolated_fused_probe_falls_back_and_all_ranks_agree(timeout):
+    """With no GPU here the isolated check fails (its ranks cannot start NCCL) or times out;
+    either way every rank of the main job gets ok = False and the same reason, so the run
+    falls back to the NCCL gather instead of hanging or crashing."""
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: the probe would really run")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_probe_worker, args=(r, 2, port, timeout, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=400) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1]
+    assert res[0]["ok"] is False
+    assert ("timed out" in res[0]["why"]) if timeout < 1 else ("rc=" in res[0]["why"])
+
+
+def test_auto_chunks():
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    per_point = 8 * 10_000 * 10  # cfg5
+    assert bench.auto_chunks(1000, 1, per_point) == 1
+    assert [bench.auto_chunks(1000, g, per_point) for g in (2, 4, 8)] == [4, 2, 1]
+    assert bench.auto_chunks(10_000, 8, 10_000) == 1  # cfg4

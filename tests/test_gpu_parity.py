@@ -304,23 +304,28 @@ def test_gl_thread_per_bin_path_all_group_shapes(gna, order):
     assert np.max(np.abs(S - Sr) / np.abs(Sr)) <= TOL_BIN
 
 
-@pytest.mark.parametrize("mode", ["mixed", "ab"])
-def test_gl_bin_value_independent_of_nbins_across_kernels(gna, mode):
-    """The lane-pair kernel (small nbins) and the thread-per-bin kernel (large nbins) form a
-    bin's value identically: 300 000 bins in one call equal the same edges in 1 000-bin
-    calls, bit for bit (mixed tier and general channel, which switch kernels by nbins)."""
-    g = synth.rng(1900)
+@pytest.mark.parametrize("order", [1, 7, 10, 13, 29, 32])
+@pytest.mark.parametrize("mode", ["fp64", "mixed", "ab"])
+def test_gl_bin_value_independent_of_nbins_across_kernels(gna, mode, order):
+    """The small-grid kernels (fp64 P_ee: node halves in two warps; mixed tier and general
+    channel: lane pairs) and the thread-per-bin kernel (large nbins) form a bin's value
+    identically: 300 000 bins in one call equal the same edges in 1 000-bin calls, bit for
+    bit, at odd and ragged orders (halves of unequal length, ragged node groups)."""
+    g = synth.rng(1900 + order)
     p = synth.random_params(g)
     edges = np.sort(g.uniform(1.0, 10.0, 300_001))
     de = _t(edges)
 
     def run(e):
         if mode == "ab":
-            return _np(gna.gl_integrate_ab(0, 1, p, 60.0, e, 10))
-        return _np(gna.gl_integrate(p, 60.0, e, 10, precision="mixed"))
+            return _np(gna.gl_integrate_ab(0, 1, p, 60.0, e, order))
+        return _np(gna.gl_integrate(p, 60.0, e, order, precision=mode))
     full = run(de)
     parts = np.concatenate([run(de[k:k + 1001]) for k in range(0, 300_000, 1000)])
     assert np.array_equal(full, parts)
+    if mode == "fp64":  # and both equal the oracle within the tier tolerance
+        Sr = oracle.gl_integrate(p, 60.0, edges[:2001], order, nthreads=_nt())
+        assert np.max(np.abs(full[:2000] - Sr) / np.abs(Sr)) <= TOL_BIN
 
 
 def test_gl_zero_mixing_is_bin_width(gna):
@@ -334,6 +339,7 @@ def test_gl_zero_mixing_is_bin_width(gna):
 def _batch_case(g, P, nbase, nbins, order):
     pts = synth.points_uniform(g, P, dict(theta12=(0.5, 0.65), theta13=(0.1, 0.2),
                                           dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3)))
+    pts = synth.invert_ordering(g, pts)  # 25 % inverted ordering
     L = g.uniform(1.0, 300.0, nbase)
     om = g.uniform(0.1, 2.0, nbase)
     edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
@@ -519,6 +525,32 @@ def test_batch_mixed_points_across_lanes_vs_oracle_and_bitwise(gna, nbase, nbins
         assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi]), (lo, hi)
 
 
+@pytest.mark.parametrize("P,nbase,nbins,order,precision", [
+    (300, 8, 1000, 10, "fp64"), (611, 1, 257, 7, "fp64"), (2003, 1, 300, 5, "fp64"),
+    (300, 8, 1000, 10, "mixed"), (611, 2, 100, 10, "mixed")])
+def test_batch_tables_valid_chunks_bitwise(gna, P, nbase, nbins, order, precision):
+    """GNA_WS_TABLES_VALID: a batch split into chunks, only the first building the node
+    tables in a shared workspace (sized for the largest chunk), gives the bits of one call
+    over all points — every kernel family (per-point, points-across-lanes, points-inner)."""
+    import torch
+    g = synth.rng(2100 + P + nbins)
+    pts, L, om, edges, data = _batch_case(g, P, nbase, nbins, order)
+    full_sp, full_x2 = _run_batch(gna, pts, L, om, edges, order, data, precision=precision)
+    de, dd = _t(edges), _t(data)
+    dp = {k: _t(v) for k, v in pts.items()}
+    sp = torch.empty((P, nbins), dtype=torch.float64, device="cuda")
+    x2 = torch.empty(P, dtype=torch.float64, device="cuda")
+    bounds = [0, P // 3, P // 3 + 1, P - 7, P]
+    biggest = max(b - a for a, b in zip(bounds, bounds[1:]))
+    ws = torch.empty(gna.oscprob_batch_workspace_size(biggest, nbase, nbins, order) // 8 + 2,
+                     dtype=torch.float64, device="cuda")
+    for c, (a, b) in enumerate(zip(bounds, bounds[1:])):
+        sub = {k: v[a:b] for k, v in dp.items()}
+        gna.oscprob_batch(sub, L, om, de, order, data=dd, spectra=sp[a:b], chi2=x2[a:b],
+                          workspace=ws, precision=precision, tables_valid=c > 0)
+    assert np.array_equal(_np(sp), full_sp) and np.array_equal(_np(x2), full_x2)
+
+
 def test_batch_single_baseline_matches_gl_integrate(gna):
     g = synth.rng(41)
     pts, _, _, edges, _ = _batch_case(g, 4, 1, 200, 10)
@@ -563,10 +595,42 @@ def test_batch_cfg5_full_size_sampled_and_split_invariant(gna):
         assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi])
 
 
+@pytest.mark.parametrize("cfg,precision", [("cfg5", "fp64"), ("cfg4", "fp64"), ("cfg5", "mixed"),
+                                           ("cfg4", "mixed")])
+def test_batch_cfg_inverted_ordering_full_size_sampled(gna, cfg, precision):
+    """cfg4 / cfg5 at full size with every dm2_31 sign-flipped (inverted ordering), in
+    the bench launch configuration (cfg5: per-point kernel; cfg4: points-across-lanes kernel),
+    sampled against the oracle at the tier tolerance; a mixed set (every 4th point flipped)
+    must give the same bits per point as the all-inverted and all-normal runs."""
+    c = synth.config(cfg)
+    inv = dict(c["points"], dm2_31=-c["points"]["dm2_31"])
+    sp, x2 = _run_batch(gna, inv, c["L_km"], c["omega"], c["edges"], c["order"], c["data"],
+                        precision=precision)
+    n = sp.shape[0]
+    idx = np.r_[0, 1, 31, 32, synth.rng(44).integers(0, n, 3), n - 1]
+    spr, x2r = oracle.batch(synth.subset_points(inv, idx), c["L_km"], c["omega"], c["edges"],
+                            c["order"], data=c["data"], nthreads=_nt())
+    tol = TOL_BIN if precision == "fp64" else TOL_MIXED
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= tol
+    bound = (_chi2_bound(spr, c["data"]) if precision == "fp64" else
+             _chi2_bound_tol(spr, c["data"], TOL_MIXED))
+    assert np.all(np.abs(x2[idx] - x2r) <= bound)
+    # mixed ordering within one call: each point's bits equal its all-one-sign run
+    flip = np.arange(n) % 4 == 1
+    mix = dict(c["points"], dm2_31=np.where(flip, -c["points"]["dm2_31"], c["points"]["dm2_31"]))
+    spm, x2m = _run_batch(gna, mix, c["L_km"], c["omega"], c["edges"], c["order"], c["data"],
+                          precision=precision)
+    assert np.array_equal(spm[flip], sp[flip]) and np.array_equal(x2m[flip], x2[flip])
+    spn, x2n = _run_batch(gna, c["points"], c["L_km"], c["omega"], c["edges"], c["order"],
+                          c["data"], precision=precision)
+    assert np.array_equal(spm[~flip], spn[~flip]) and np.array_equal(x2m[~flip], x2n[~flip])
+
+
 # ------------------------------------------------------------------------ NEXT-1 separable scan
 def _scan_case(g, nmix, nmass, nbase, nbins, order):
     grid = dict(theta12=g.uniform(0.5, 0.65, nmix), theta13=g.uniform(0.1, 0.2, nmix),
                 dm2_21=g.uniform(6e-5, 9e-5, nmass), dm2_31=g.uniform(2.2e-3, 2.8e-3, nmass))
+    grid = synth.invert_ordering(g, grid)  # 25 % inverted mass points (DESIGN.md §5, S:328)
     L = g.uniform(1.0, 300.0, nbase)
     om = g.uniform(0.1, 2.0, nbase)
     edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
@@ -591,8 +655,10 @@ def test_scan_vs_oracle_on_expanded_grid(gna, nmix, nmass, nbase, nbins, order):
     assert np.max(np.abs(sp - spb) / np.abs(spb)) <= 1e-13
 
 
-def test_scan_cfg4grid_full_size_sampled(gna):
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_scan_cfg4grid_full_size_sampled(gna, sign):
     c = synth.config("cfg4grid")
+    c["grid"]["dm2_31"] = sign * c["grid"]["dm2_31"]  # -1: inverted ordering
     sp, x2 = gna.oscprob_scan({k: _t(v) for k, v in c["grid"].items()}, c["L_km"], c["omega"],
                               _t(c["edges"]), c["order"], data=_t(c["data"]))
     sp, x2 = _np(sp).reshape(-1, c["edges"].size - 1), _np(x2).ravel()
@@ -801,8 +867,9 @@ def test_fused_gather_epilogue_single_rank(gna, P, nbase):
 
 
 # ------------------------------------------------------------------------ on-GPU fit loop
-def _fit_case():
-    truth = np.array([0.5838, 0.1496, 7.53e-5, 2.52e-3])
+def _fit_case(sign=1.0):
+    # sign = -1: inverted-ordering truth (signed dm2_31)
+    truth = np.array([0.5838, 0.1496, 7.53e-5, sign * 2.52e-3])
     L, om = np.array([52.5, 53.0]), np.array([1.0, 0.98])
     edges = synth.uniform_edges(500, 1.0, 10.0)
     pts = dict(theta12=truth[:1], theta13=truth[1:2], dm2_21=truth[2:3], dm2_31=truth[3:4])
@@ -810,8 +877,9 @@ def _fit_case():
     return truth, L, om, edges, data[0]
 
 
-def test_fit_pattern_search_recovers_truth(gna):
-    truth, L, om, edges, data = _fit_case()
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_fit_pattern_search_recovers_truth(gna, sign):
+    truth, L, om, edges, data = _fit_case(sign)
     step = np.array([0.01, 0.005, 2e-6, 5e-5])
     # start inside the truth's basin (chi^2 in dm2_31 is multimodal: the fast oscillation)
     start = truth + np.array([0.7, -0.6, 0.8, -0.5]) * step
@@ -823,12 +891,14 @@ def test_fit_pattern_search_recovers_truth(gna):
     assert np.all(np.abs(x - truth) <= 1e-6 * np.abs(truth)), (x, truth)
 
 
-def test_fit_pattern_search_steps_match_host_compass_search_on_oracle_chi2(gna):
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+def test_fit_pattern_search_steps_match_host_compass_search_on_oracle_chi2(gna, sign):
     """Each GPU iteration (niter = 1 calls) equals one compass step computed on the host:
     the 81 candidates centre + step * {-1, 0, 1}^4 (first coordinate fastest), their chi^2 from
     the oracle, argmin with ties to the lowest index; move there if it beats the centre, else
-    halve the steps.  The state after every step must match bit for bit."""
-    truth, L, om, edges, data = _fit_case()
+    halve the steps.  The state after every step must match bit for bit (normal and inverted
+    ordering)."""
+    truth, L, om, edges, data = _fit_case(sign)
     step = np.array([0.01, 0.005, 2e-6, 5e-5])
     st = np.r_[truth + np.array([0.7, -0.6, 0.8, -0.5]) * step, step]
     de, dd = _t(edges), _t(data)

@@ -20,7 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=None)
     ap.add_argument("--tag", default="base")
-    ap.add_argument("--mode", default="fp64", choices=["fp64", "mixed", "ab"])
+    ap.add_argument("--mode", default="fp64", choices=["fp64", "mixed", "ab", "eval"])
     ap.add_argument("--cases", default="100:5,100000:10,1000000:10", help="nbins:order,...")
     a = ap.parse_args()
     gna.load(a.lib)
@@ -28,7 +28,13 @@ def main():
     for nbins, order in [tuple(int(v) for v in c.split(":")) for c in a.cases.split(",")]:
         edges = torch.tensor(synth.uniform_edges(nbins), dtype=torch.float64, device=dev)
         out = torch.empty(nbins, dtype=torch.float64, device=dev)
-        if a.mode == "ab":
+        if a.mode == "eval":  # nbins = number of energies (elementwise P_ee), order ignored
+            E = torch.linspace(1.0, 10.0, nbins, dtype=torch.float64, device=dev)
+
+            def call():
+                gna.oscprob_eval(synth.CANONICAL, 52.5, E, out=out)
+            order = 1
+        elif a.mode == "ab":
             def call():
                 gna.gl_integrate_ab(0, 1, synth.CANONICAL, 52.5, edges, order, out=out)
         else:

@@ -40,6 +40,13 @@ VARIANTS = {
     "mb20_nt3": dict(GNA_BATCH_MINB=20, GNA_BATCH_PI_MINB=1, GNA_BATCH_PI_NT=1),
     "pi_nt3_m16": dict(GNA_BATCH_PI_NT=1, GNA_BATCH_PI_MINB=16),
     "pi_m20_w240": dict(GNA_BATCH_PI_MINB=20, GNA_BATCH_PPW_WORK=240),
+    "gl_nosplit": dict(GNA_GL_SPLIT=0),
+    "nopdl_single": dict(GNA_PDL_SINGLE=0),
+    "nopdl_single_nosplit": dict(GNA_PDL_SINGLE=0, GNA_GL_SPLIT=0),
+    "gl_nosplit_tb64": dict(GNA_GL_SPLIT=0, GNA_GL_TB_THREADS=64, GNA_GL_TB_MINB=8),
+    "gl_split_bw2": dict(GNA_GL_SPLIT_BW=2, GNA_GL_SPLIT_MINB=4),
+    "gl_split_mb21": dict(GNA_GL_SPLIT_MINB=21),
+    "gl_split_mb16": dict(GNA_GL_SPLIT_MINB=16),
     "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
     "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
     "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
@@ -49,7 +56,8 @@ VARIANTS = {
 KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb0E",
            r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
            r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E",
-           r"k_oscprob_batchILi1ELi10ELi0ELb1E"]
+           r"k_oscprob_batchILi1ELi10ELi0ELb1E", r"k_gl_integrate_splitILi10EN3gna7PeeCoef",
+           r"k_gl_integrate_tbILi10EN3gna7PeeCoef"]
 
 
 def main(names):
