@@ -723,6 +723,9 @@ def main():
         if world > 1:
             _barrier(dist, args, local)
 
+    # live FP64 denominator check: DFMA issue rate of this GPU (outside the timed region)
+    fp64_probe = run_fp64_probe(local) if rank == 0 else None
+
     # ---------------- warm-up
     for _ in range(max(args.warmup, 3)):
         flush.zero_()
@@ -829,10 +832,17 @@ def main():
         achieved = launch_units * ops_eval / (kern_avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
                 "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
-                "peak_source": "148 SM x 64 FP64 lanes x sm_max clock (lanes measured by "
-                               "tools/probe_fp64.cu: 18.55 T DFMA/s at 1965 MHz)",
+                "peak_source": "148 SM x 64 FP64 lanes x sm_max clock (DESIGN.md §6; the lane "
+                               "count is measured: fp64_probe below)",
                 "ops_per_energy_point": ops_eval, "sin2_poly_degree": deg,
-                "kernel_ms_per_launch": kern_avg_ms}
+                "kernel_ms_per_launch": kern_avg_ms,
+                # the same time on the other basis: SURVEY §8(d)'s ~50 FP64 instructions per
+                # energy point (its estimate before the 12-op sin^2 of DESIGN.md §6.1)
+                "bases": {"executed_%d_ops" % ops_eval: achieved * 1e12 / peak_ops,
+                          "survey_50_ops": launch_units * 50 / (kern_avg_ms * 1e-3) / peak_ops}}
+        if fp64_probe:
+            roof["fp64_probe"] = fp64_probe
+            roof["frac_of_probe"] = achieved * 1e3 / fp64_probe["dfma_G_per_s"]
         if args.precision == "mixed":
             # NEXT-3 mixed tier: the work spreads over the FP64, XU and FMA
             # pipes, so the roofline is instruction issue (1 warp instruction per SMSP per cycle
@@ -958,6 +968,25 @@ def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
     return bool(float(ok) == 1.0)
 
 
+def run_fp64_probe(local: int):
+    """build/probe_fp64 (tools/probe_fp64.cu, built by __graft_entry__.build()) in DFMA-only
+    mode on this rank's GPU: 148 x 8 blocks x 256 threads of 8 independent DFMA chains, best
+    of 5; returns its rate and the SM clock it saw, or None when the binary is absent."""
+    exe = os.path.join(ROOT, "build", "probe_fp64")
+    if not os.path.exists(exe):
+        return None
+    env = dict(os.environ, PROBE_DFMA_ONLY="1", CUDA_VISIBLE_DEVICES=str(_smi_index(local)))
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60, env=env).stdout
+        rows = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+        d = next(r for r in rows if r.get("probe") == "dfma")
+        dev = rows[0]
+        return {"dfma_G_per_s": d["Gops_per_s"], "clock_khz": dev.get("clock_khz"),
+                "source": "build/probe_fp64 (tools/probe_fp64.cu), run before the timed region"}
+    except (OSError, subprocess.SubprocessError, StopIteration, ValueError, KeyError):
+        return None
+
+
 def _barrier(dist, args, local):
     if args.backend == "nccl":
         dist.barrier(device_ids=[local])
@@ -998,11 +1027,15 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory()
         return t, t.numpy()
 
+    host_note = None
     if args.workload in ("cfg4", "cfg5"):
+        from types import SimpleNamespace
+
         from paper_1804_07682_b200 import dist as gdist
         P = c["points"]["theta12"].size
         nb = c["edges"].size - 1
-        lo, hi = gdist.shard_range(P, world, rank)
+        sb = gdist.ShardedBatch(P, nb, world, rank)
+        lo, hi = sb.lo, sb.hi
         keep = []
         pts = {}
         for k, v in c["points"].items():
@@ -1011,23 +1044,48 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
             pts[k] = a
         te, edges = pinned(c["edges"])
         td, data = pinned(c["data"])
-        ts, spectra = pinned(np.empty((hi - lo, nb)))
-        tx, chi2 = pinned(np.empty(hi - lo))
-        keep += [te, td, ts, tx]
+        keep += [te, td]
+        out = None
+        if world > 1:
+            # the node's host memory receives every rank's rows (shared, page-locked)
+            try:
+                out = gdist.NodeSharedHost({"spectra": (P, nb), "chi2": (P,)}, rank,
+                                           dist.distributed_c10d._get_default_store())
+                host_note = "spectra + chi2 of all points gathered into one node-shared host buffer"
+            except Exception as exc:  # noqa: BLE001 — e.g. a small /dev/shm
+                out = None
+                host_note = "per-rank pinned buffers (node-shared buffer unavailable: %s)" % (
+                    str(exc).splitlines()[0][:100] if str(exc) else type(exc).__name__)
+            ok = torch.tensor([1.0 if out is not None else 0.0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if float(ok) != 1.0 and out is not None:
+                out.close()
+                out = None
+        if out is None:
+            ts, spectra = pinned(np.empty((P, nb)))
+            tx, chi2 = pinned(np.empty(P))
+            keep += [ts, tx]
+            out = SimpleNamespace(arrays={"spectra": spectra, "chi2": chi2})
+
+        def bar():
+            if world > 1:
+                _barrier(dist, args, local)
 
         def one():
-            # the fit step a minimiser makes: inputs H2D, chi^2 per point D2H (the "loss")
-            gna.oscprob_batch_host(pts, c["L_km"], c["omega"], edges, c["order"], data=data,
-                                   spectra=False, chi2=chi2)
+            # the declared outputs: per step the points, edges and data go H2D, the spectra
+            # and chi^2 of every point come back D2H into host memory (gathered at N > 1)
+            gdist.oscprob_batch_host_sharded(sb, pts, c["L_km"], c["omega"], edges, c["order"],
+                                             data, out, bar)
 
-        def one_spectra():
-            # the same call also returning the 80 MB of spectra (PCIe D2H-bound)
-            gna.oscprob_batch_host(pts, c["L_km"], c["omega"], edges, c["order"], data=data,
-                                   spectra=spectra, chi2=chi2)
+        def one_fit():
+            # the fit step a minimiser makes: only chi^2 per point comes back (the "loss")
+            gdist.oscprob_batch_host_sharded(sb, pts, c["L_km"], c["omega"], edges, c["order"],
+                                             data, out, bar, spectra=False)
 
-        h2d = 4 * (hi - lo) * 8 + edges.nbytes + data.nbytes
-        d2h = chi2.nbytes
-        d2h_spectra = spectra.nbytes + chi2.nbytes
+        # bytes summed over the ranks
+        h2d = 4 * P * 8 + world * (edges.nbytes + data.nbytes)
+        d2h = P * nb * 8 + P * 8
+        d2h_fit = P * 8
         units = (hi - lo) * c["L_km"].size * nb * c["order"]
     elif args.workload in ("cfg1", "cfg2"):
         te, edges = pinned(c["edges"])
@@ -1076,8 +1134,8 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
     total_units = units * world if args.workload in ("cfg1", "cfg2", "cfg3") else c["evals"]
     extra = {}
     if args.workload in ("cfg4", "cfg5"):
-        # second measurement: the call that also reads the spectra back
-        one_spectra()
+        # second measurement: the chi^2-only fit step
+        one_fit()
         torch.cuda.synchronize()
         if world > 1:
             _barrier(dist, args, local)
@@ -1085,19 +1143,26 @@ def e2e(args, c, gna, torch, dist, dev, world, rank, local):
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(steps):
-            one_spectra()
+            one_fit()
         f1.record()
         torch.cuda.synchronize()
         ms2 = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(ms2, op=dist.ReduceOp.MAX)
-        extra["with_spectra"] = {"value": total_units * steps / (float(ms2[0]) * 1e-3),
-                                 "h2d_bytes_per_step": int(h2d),
-                                 "d2h_bytes_per_step": int(d2h_spectra)}
+        extra["fit_step"] = {"value": total_units * steps / (float(ms2[0]) * 1e-3),
+                             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h_fit),
+                             "outputs": "chi2 per point only"}
+        extra["outputs"] = "spectra + chi2 of every point in host memory"
+        if host_note:
+            extra["host_gather"] = host_note
+        if world > 1 and hasattr(out, "close"):
+            out.close(barrier=lambda: _barrier(dist, args, local))
     del keep
     return {"value": total_units * steps / (float(ms[0]) * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), **extra,
-            "steps": steps, "api": "gna_oscprob_batch_host (chi2 read back; with_spectra: + spectra)" if args.workload in ("cfg4", "cfg5")
+            "steps": steps, "api": ("dist.oscprob_batch_host_sharded -> gna_oscprob_batch_host "
+                                    "per rank (H2D inputs, kernels, D2H spectra + chi2), barrier")
+            if args.workload in ("cfg4", "cfg5")
             else ("gna_gl_integrate_host" if args.workload == "cfg2" else
                   ("gna_oscprob_eval_host + gna_gl_integrate_host" if args.workload == "cfg1"
                    else "gna_oscprob_eval_host"))}

@@ -47,8 +47,10 @@
  *     staging allocation failed.  Preconditions NOT checked on the device
  *     (violations give unspecified values, never a fault): E > 0,
  *     edges strictly increasing, data > 0.
- *   Domain: phases |Delta| <= 2^40 rad are reduced exactly; the result is
- *     accurate to the rounding of Delta itself (R7, R9).
+ *   Domain: phases with |y| = |2 Delta / pi| < 2^51, i.e. |Delta| < pi * 2^50
+ *     (about 3.5e15 rad), are reduced exactly (the magic-number rint of y is an
+ *     exact integer there); the result is accurate to the rounding of Delta
+ *     itself (R7, R9, R10).
  *   Thread safety: stateless and re-entrant for the device entry points;
  *     concurrent calls on disjoint outputs are allowed.  The *_host
  *     entry points serialise on an internal lock per device (calls on different
@@ -289,9 +291,14 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
  * datasets are divided into smaller sizes to organize overlapped execution,
  * asynchronous memory copying").  Same arithmetic as the device entry points
  * (bitwise identical results); inputs are copied host->device and results
- * device->host in chunks so that the copies overlap the kernels.  chunk = 0
- * picks a default (batch: ~8 MiB of spectra per chunk, or a single chunk when
- * only chi^2 is requested).  Returns after the results are in host memory.
+ * device->host in chunks on three library-owned streams (H2D, compute, D2H; a
+ * ring of three chunk slots ordered by events), so chunk c's D2H and chunk c+2's
+ * H2D overlap chunk c+1's kernel while every kernel has the whole GPU.  chunk = 0
+ * picks a default (eval: 4 Mi energies, GL: 1 Mi bins, batch: ~8 MiB of spectra
+ * per chunk, or a single chunk when only chi^2 is requested; the batch uploads all
+ * points and builds the node tables once per call).  Pinned (page-locked) host
+ * arrays give full PCIe speed; pageable ones work but copy synchronously.
+ * Returns after the results are in host memory (also on error).
  * ------------------------------------------------------------------------- */
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,
                           double* h_P, int64_t chunk, void* stream);

@@ -442,7 +442,7 @@ def fit_pattern_search(state, L_km, omega, edges, order: int, data, niter: int, 
 # ---------------------------------------------------------------- host-buffer entry points
 def oscprob_eval_host(params, L_km: float, E: np.ndarray, out: np.ndarray | None = None,
                       chunk: int = 0, stream=None) -> np.ndarray:
-    """P_ee over a HOST energy array: chunked H2D / kernel / D2H on two streams."""
+    """P_ee over a HOST energy array: chunked H2D / kernel / D2H on three streams (copies overlap kernels)."""
     L = load()
     E = _host(E, "E")
     if out is None:

@@ -53,6 +53,19 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     return target
 
 
+PROBE_SRC = os.path.join(ROOT, "tools", "probe_fp64.cu")
+PROBE_BIN = os.path.join(ROOT, "build", "probe_fp64")
+
+
+def build_probe() -> str:
+    """FP64-pipe microbenchmark executable (measurement tooling, not the product)."""
+    os.makedirs(os.path.dirname(PROBE_BIN), exist_ok=True)
+    if not os.path.exists(PROBE_BIN) or os.path.getmtime(PROBE_BIN) < os.path.getmtime(PROBE_SRC):
+        subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                               "-o", PROBE_BIN, PROBE_SRC])
+    return PROBE_BIN
+
+
 if __name__ == "__main__":
     import sys
     print(build(force=True, verbose="-v" in sys.argv))

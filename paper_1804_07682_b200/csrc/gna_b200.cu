@@ -525,14 +525,18 @@ int launch_eval(const Coef& c, const double* E, int64_t n, double* P, cudaStream
 // ----------------------------------------------------------------------------
 // staging for the *_host entry points (library-owned, per device)
 // ----------------------------------------------------------------------------
+// Three streams per device: 0 = H2D, 1 = compute, 2 = D2H, and a ring of kRing chunk
+// slots whose reuse is ordered by events, so chunk c's D2H, chunk c+1's kernel and chunk
+// c+2's H2D run at the same time (the paper's "CUDA Streams ... overlapped execution,
+// asynchronous memory copying") while every kernel still gets the whole GPU.
+constexpr int kRing = 3;
 struct Staging {
   bool init = false;
-  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_in = nullptr;
-  void* buf[2] = {nullptr, nullptr};  // per-stream chunk buffers
-  size_t cap[2] = {0, 0};
-  void* shared = nullptr;             // per-call shared inputs (edges, data)
-  size_t shared_cap = 0;
+  cudaEvent_t ev_h[kRing] = {}, ev_k[kRing] = {}, ev_d[kRing] = {};
+  void* buf = nullptr;  // one device allocation, carved per call
+  size_t cap = 0;
 };
 
 std::mutex g_stage_mu[128];  // one lock per device: host-buffer calls on different GPUs overlap
@@ -558,14 +562,69 @@ int ensure(void** p, size_t* cap, size_t need) {
 int stage_init(Staging* S) {
   if (S->init) return GNA_OK;
   cudaError_t e;
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     e = cudaStreamCreateWithFlags(&S->st[i], cudaStreamNonBlocking);
     if (e != cudaSuccess) return cuda_fail(e);
   }
-  e = cudaEventCreateWithFlags(&S->ev_in, cudaEventDisableTiming);
-  if (e != cudaSuccess) return cuda_fail(e);
+  cudaEvent_t* evs[1 + 3 * kRing];
+  int n = 0;
+  evs[n++] = &S->ev_in;
+  for (int r = 0; r < kRing; ++r) {
+    evs[n++] = &S->ev_h[r];
+    evs[n++] = &S->ev_k[r];
+    evs[n++] = &S->ev_d[r];
+  }
+  for (int i = 0; i < n; ++i) {
+    e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
   S->init = true;
   return GNA_OK;
+}
+
+// Chunk pipeline of the host-buffer entry points: H2D(ci) on st[0] -> kernel(ci) on st[1]
+// -> D2H(ci) on st[2], chunk ci in ring slot ci % kRing.  A slot's input is overwritten only
+// after the kernel of chunk ci - kRing has read it, and its output only after the D2H of
+// chunk ci - kRing has copied it out.  Waits for the caller's stream first; returns after
+// all three streams are idle (also on error, so no copy outlives the call).
+template <class FH, class FK, class FD>
+int run_pipeline(Staging* S, cudaStream_t caller, int64_t nchunks, FH h2d, FK kern, FD d2h) {
+  cudaError_t e = cudaSuccess;
+  int rc = GNA_OK;
+  auto fail = [&](int code) {
+    for (int i = 0; i < 3; ++i) cudaStreamSynchronize(S->st[i]);
+    return code;
+  };
+  if ((e = cudaEventRecord(S->ev_in, caller)) != cudaSuccess) return cuda_fail(e);
+  for (int i = 0; i < 3; ++i)
+    if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int r = (int)(ci % kRing);
+    const bool reuse = ci >= kRing;
+    if (reuse && (e = cudaStreamWaitEvent(S->st[0], S->ev_k[r], 0)) != cudaSuccess) break;
+    if ((rc = h2d(ci, r, S->st[0]))) return fail(rc);
+    if ((e = cudaEventRecord(S->ev_h[r], S->st[0])) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(S->st[1], S->ev_h[r], 0)) != cudaSuccess) break;
+    if (reuse && (e = cudaStreamWaitEvent(S->st[1], S->ev_d[r], 0)) != cudaSuccess) break;
+    if ((rc = kern(ci, r, S->st[1]))) return fail(rc);
+    if ((e = cudaEventRecord(S->ev_k[r], S->st[1])) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(S->st[2], S->ev_k[r], 0)) != cudaSuccess) break;
+    if ((rc = d2h(ci, r, S->st[2]))) return fail(rc);
+    if ((e = cudaEventRecord(S->ev_d[r], S->st[2])) != cudaSuccess) break;
+  }
+  if (e != cudaSuccess) return fail(cuda_fail(e));
+  for (int i = 0; i < 3; ++i)
+    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return fail(cuda_fail(e));
+  return GNA_OK;
+}
+
+int h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
 
 }  // namespace
@@ -661,32 +720,25 @@ int gna_gl_integrate_host(const gna_osc_params* p, double L_km, const double* h_
   if ((rc = stage_init(S))) return rc;
   if (chunk <= 0) chunk = (int64_t)1 << 20;  // bins per chunk
   if (chunk > nbins) chunk = nbins;
-  const size_t need = (size_t)(2 * chunk + 2) * 8;  // edges (chunk+1) + bins (chunk), aligned
-  for (int i = 0; i < 2; ++i)
-    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  // slot r: edges (chunk + 1, padded to chunk + 2) then bins (chunk)
+  const size_t slot = (size_t)(2 * chunk + 2);
+  if ((rc = ensure(&S->buf, &S->cap, kRing * slot * 8))) return rc;
+  double* base = (double*)S->buf;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  cudaError_t e = cudaEventRecord(S->ev_in, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e);
-  for (int i = 0; i < 2; ++i)
-    if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
   const int64_t nchunks = (nbins + chunk - 1) / chunk;
-  for (int64_t ci = 0; ci < nchunks; ++ci) {
-    const int si = (int)(ci & 1);
-    cudaStream_t s = S->st[si];
-    const int64_t o = ci * chunk;
-    const int64_t m = (o + chunk <= nbins) ? chunk : nbins - o;
-    double* dEd = (double*)S->buf[si];
-    double* dB = dEd + chunk + 2;
-    if ((e = cudaMemcpyAsync(dEd, h_edges + o, (size_t)(m + 1) * 8, cudaMemcpyHostToDevice, s)))
-      return cuda_fail(e);
-    if ((rc = launch_gl(c, dEd, m, order, dB, s))) return rc;
-    if ((e = cudaMemcpyAsync(h_bins + o, dB, (size_t)m * 8, cudaMemcpyDeviceToHost, s)))
-      return cuda_fail(e);
-  }
-  for (int i = 0; i < 2; ++i)
-    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
-  return GNA_OK;
+  auto rows = [&](int64_t ci) { return std::min<int64_t>(chunk, nbins - ci * chunk); };
+  return run_pipeline(
+      S, (cudaStream_t)stream, nchunks,
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return h2d_copy(base + r * slot, h_edges + ci * chunk, (size_t)(rows(ci) + 1) * 8, s);
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return launch_gl(c, base + r * slot, rows(ci), order, base + r * slot + chunk + 2, s);
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return d2h_copy(h_bins + ci * chunk, base + r * slot + chunk + 2, (size_t)rows(ci) * 8, s);
+      });
 }
 
 size_t gna_oscprob_batch_workspace_size(int64_t npoints, int32_t nbase, int64_t nbins,
@@ -883,32 +935,24 @@ int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_
   if (chunk <= 0) chunk = (int64_t)1 << 22;  // 4 Mi elements = 32 MiB per direction
   if (chunk > n) chunk = n;
   chunk = (chunk + 1) & ~(int64_t)1;         // keep the double2 path aligned
-  const size_t need = (size_t)chunk * 16;    // E and P halves
-  for (int i = 0; i < 2; ++i)
-    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
+  const size_t slot = (size_t)chunk * 2;     // E then P
+  if ((rc = ensure(&S->buf, &S->cap, kRing * slot * 8))) return rc;
+  double* base = (double*)S->buf;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  cudaError_t e = cudaEventRecord(S->ev_in, (cudaStream_t)stream);
-  if (e != cudaSuccess) return cuda_fail(e);
-  for (int i = 0; i < 2; ++i)
-    if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
-  int64_t nchunks = (n + chunk - 1) / chunk;
-  for (int64_t ci = 0; ci < nchunks; ++ci) {
-    const int si = (int)(ci & 1);
-    cudaStream_t s = S->st[si];
-    const int64_t o = ci * chunk;
-    const int64_t m = (o + chunk <= n) ? chunk : n - o;
-    double* dE = (double*)S->buf[si];
-    double* dP = dE + chunk;
-    if ((e = cudaMemcpyAsync(dE, h_E + o, (size_t)m * 8, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-      return cuda_fail(e);
-    if ((rc = launch_eval(c, dE, m, dP, s))) return rc;
-    if ((e = cudaMemcpyAsync(h_P + o, dP, (size_t)m * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
-      return cuda_fail(e);
-  }
-  for (int i = 0; i < 2; ++i)
-    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
-  return GNA_OK;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  auto len = [&](int64_t ci) { return std::min<int64_t>(chunk, n - ci * chunk); };
+  return run_pipeline(
+      S, (cudaStream_t)stream, nchunks,
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return h2d_copy(base + r * slot, h_E + ci * chunk, (size_t)len(ci) * 8, s);
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return launch_eval(c, base + r * slot, len(ci), base + r * slot + chunk, s);
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        return d2h_copy(h_P + ci * chunk, base + r * slot + chunk, (size_t)len(ci) * 8, s);
+      });
 }
 
 int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, const double* omega,
@@ -926,74 +970,67 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   if ((rc = stage_init(S))) return rc;
   const int64_t P = h_pts->npoints;
   if (chunk_points <= 0) {
-    // ~8 MiB of spectra per chunk (their D2H overlaps the next chunk's kernels), at least 1
+    // ~8 MiB of spectra per chunk (their D2H overlaps the next chunks' kernels), at least 1
     // point; without spectra there is nothing large to overlap: one launch over all points
-    // (chunking would only add per-chunk launches and partial last waves)
     chunk_points = h_spectra ? ((int64_t)8 << 20) / (nbins * 8) : P;
     if (chunk_points < 1) chunk_points = 1;
   }
   if (chunk_points > P) chunk_points = P;
-  // per-stream chunk buffer: workspace (16-aligned, first) + 4 param arrays + spectra + chi2
-  const size_t ws_bytes = batch_ws_bytes(chunk_points, nbase, nbins, order, h_chi2 != nullptr);
-  const size_t n_ws = ws_bytes / 8;
-  const size_t n_par = 4 * (size_t)chunk_points;
-  const size_t n_spec = h_spectra ? (size_t)chunk_points * nbins : 0;
-  const size_t n_chi = h_chi2 ? (size_t)chunk_points : 0;
-  const size_t need = (n_ws + n_par + n_spec + n_chi) * 8;
-  for (int i = 0; i < 2; ++i)
-    if ((rc = ensure(&S->buf[i], &S->cap[i], need))) return rc;
-  // shared by the chunks: node tables (built once per call, 16-aligned, first), edges, data
+  // device layout (16-byte aligned pieces): node tables | edges | data | points [4][P] |
+  // chi2 [P] | workspace (one chunk) | kRing spectra slots (one chunk each)
   const size_t tb = batch_tables_bytes(nbins, order);
-  const size_t n_shared = (size_t)(nbins + 1) + (h_data ? (size_t)nbins : 0);
-  if ((rc = ensure(&S->shared, &S->shared_cap, tb + n_shared * 8))) return rc;
-  double* d_tables = (double*)S->shared;
-  double* d_edges = (double*)((char*)S->shared + tb);
-  double* d_data = h_data ? d_edges + (nbins + 1) : nullptr;
-
-  cudaError_t e;
-  cudaStream_t s0 = S->st[0];
-  if ((e = cudaEventRecord(S->ev_in, (cudaStream_t)stream)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaStreamWaitEvent(s0, S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaMemcpyAsync(d_edges, h_edges, (size_t)(nbins + 1) * 8, cudaMemcpyHostToDevice, s0)))
-    return cuda_fail(e);
-  if (d_data &&
-      (e = cudaMemcpyAsync(d_data, h_data, (size_t)nbins * 8, cudaMemcpyHostToDevice, s0)))
-    return cuda_fail(e);
-  if ((rc = launch_batch_tables(d_edges, nbins, order, d_tables, s0))) return rc;
-  if ((e = cudaEventRecord(S->ev_in, s0)) != cudaSuccess) return cuda_fail(e);
-  if ((e = cudaStreamWaitEvent(S->st[1], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
-
+  const size_t b_edges = align16((size_t)(nbins + 1) * 8);
+  const size_t b_data = h_data ? align16((size_t)nbins * 8) : 0;
+  const size_t b_pts = align16((size_t)4 * P * 8);
+  const size_t b_chi = h_chi2 ? align16((size_t)P * 8) : 0;
+  const size_t b_ws = batch_ws_bytes(chunk_points, nbase, nbins, order, h_chi2 != nullptr);
+  const size_t b_slot = h_spectra ? align16((size_t)chunk_points * nbins * 8) : 0;
+  if ((rc = ensure(&S->buf, &S->cap, tb + b_edges + b_data + b_pts + b_chi + b_ws + kRing * b_slot)))
+    return rc;
+  char* q = (char*)S->buf;
+  double* d_tables = (double*)q;
+  q += tb;
+  double* d_edges = (double*)q;
+  q += b_edges;
+  double* d_data = h_data ? (double*)q : nullptr;
+  q += b_data;
+  double* d_pts = (double*)q;
+  q += b_pts;
+  double* d_chi = h_chi2 ? (double*)q : nullptr;
+  q += b_chi;
+  void* d_ws = q;
+  q += b_ws;
+  char* d_slots = q;
   const double* hsrc[4] = {h_pts->theta12, h_pts->theta13, h_pts->dm2_21, h_pts->dm2_31};
   const int64_t nchunks = (P + chunk_points - 1) / chunk_points;
-  for (int64_t ci = 0; ci < nchunks; ++ci) {
-    const int si = (int)(ci & 1);
-    cudaStream_t s = S->st[si];
-    const int64_t o = ci * chunk_points;
-    const int64_t m = (o + chunk_points <= P) ? chunk_points : P - o;
-    double* base = (double*)S->buf[si];
-    void* dws = base;
-    double* dpar = base + n_ws;
-    double* dspec = h_spectra ? dpar + n_par : nullptr;
-    double* dchi = h_chi2 ? dpar + n_par + n_spec : nullptr;
-    for (int a = 0; a < 4; ++a)
-      if ((e = cudaMemcpyAsync(dpar + a * chunk_points, hsrc[a] + o, (size_t)m * 8,
-                               cudaMemcpyHostToDevice, s)))
-        return cuda_fail(e);
-    gna_param_batch dp = {dpar, dpar + chunk_points, dpar + 2 * chunk_points,
-                          dpar + 3 * chunk_points, m};
-    if ((rc = launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data, dchi,
-                           dws, s, kOutLocal, false, d_tables)))
-      return rc;
-    if (h_spectra && (e = cudaMemcpyAsync(h_spectra + o * nbins, dspec, (size_t)m * nbins * 8,
-                                          cudaMemcpyDeviceToHost, s)))
-      return cuda_fail(e);
-    if (h_chi2 &&
-        (e = cudaMemcpyAsync(h_chi2 + o, dchi, (size_t)m * 8, cudaMemcpyDeviceToHost, s)))
-      return cuda_fail(e);
-  }
-  for (int i = 0; i < 2; ++i)
-    if ((e = cudaStreamSynchronize(S->st[i])) != cudaSuccess) return cuda_fail(e);
-  return GNA_OK;
+  auto rows = [&](int64_t ci) { return std::min<int64_t>(chunk_points, P - ci * chunk_points); };
+  return run_pipeline(
+      S, (cudaStream_t)stream, nchunks,
+      [&](int64_t ci, int, cudaStream_t s) {
+        if (ci > 0) return (int)GNA_OK;  // every input goes up with the first chunk
+        int r2 = h2d_copy(d_edges, h_edges, (size_t)(nbins + 1) * 8, s);
+        if (!r2 && d_data) r2 = h2d_copy(d_data, h_data, (size_t)nbins * 8, s);
+        for (int a = 0; a < 4 && !r2; ++a) r2 = h2d_copy(d_pts + a * P, hsrc[a], (size_t)P * 8, s);
+        return r2;
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        int r2 = GNA_OK;
+        if (ci == 0 && (r2 = launch_batch_tables(d_edges, nbins, order, d_tables, s))) return r2;
+        const int64_t o = ci * chunk_points, m = rows(ci);
+        const gna_param_batch dp = {d_pts + o, d_pts + P + o, d_pts + 2 * P + o,
+                                    d_pts + 3 * P + o, m};
+        return launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order,
+                            h_spectra ? (double*)(d_slots + r * b_slot) : nullptr, d_data,
+                            d_chi ? d_chi + o : nullptr, d_ws, s, kOutLocal, false, d_tables);
+      },
+      [&](int64_t ci, int r, cudaStream_t s) {
+        const int64_t o = ci * chunk_points, m = rows(ci);
+        int r2 = GNA_OK;
+        if (h_spectra)
+          r2 = d2h_copy(h_spectra + o * nbins, d_slots + r * b_slot, (size_t)m * nbins * 8, s);
+        if (!r2 && h_chi2) r2 = d2h_copy(h_chi2 + o, d_chi + o, (size_t)m * 8, s);
+        return r2;
+      });
 }
 
 void gna_release(void) {
@@ -1002,18 +1039,19 @@ void gna_release(void) {
   for (int d = 0; d < 128; ++d) {
     std::lock_guard<std::mutex> lk(g_stage_mu[d]);
     Staging* S = &g_stage[d];
-    if (!S->init && !S->buf[0] && !S->buf[1] && !S->shared) continue;
+    if (!S->init && !S->buf) continue;
     cudaSetDevice(d);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i)
       if (S->st[i]) cudaStreamSynchronize(S->st[i]);
-      if (S->buf[i]) cudaFree(S->buf[i]);
+    if (S->buf) cudaFree(S->buf);
+    for (int i = 0; i < 3; ++i)
       if (S->st[i]) cudaStreamDestroy(S->st[i]);
-      S->buf[i] = nullptr;
-      S->cap[i] = 0;
-      S->st[i] = nullptr;
-    }
-    if (S->shared) cudaFree(S->shared);
     if (S->ev_in) cudaEventDestroy(S->ev_in);
+    for (int r = 0; r < kRing; ++r) {
+      if (S->ev_h[r]) cudaEventDestroy(S->ev_h[r]);
+      if (S->ev_k[r]) cudaEventDestroy(S->ev_k[r]);
+      if (S->ev_d[r]) cudaEventDestroy(S->ev_d[r]);
+    }
     *S = Staging();
   }
   cudaSetDevice(cur);

@@ -10,8 +10,9 @@
 //   acc += w * ((-1)^q v)       DFMA  (sign of v flipped with 2 integer ops on its hi word)
 // = 12 (13) FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
 // v(f) = -cos(pi f)/2, so that sum_ij w_ij sin^2 = sum w_ij / 2 + sum w_ij (-1)^q v.
-// The reduction is exact for |y| < 2^51; the only error beyond the polynomial's is
-// the rounding of kq and invE (R7, R9).
+// The reduction is exact for |y| < 2^51, i.e. |Delta| < pi * 2^50 (t then lies in
+// [2^52, 2^53), where the ulp is 1 and t's low mantissa bit is the parity of q); the only
+// error beyond the polynomial's is the rounding of kq and invE (R7, R9, R10).
 #pragma once
 #include <cstdint>
 

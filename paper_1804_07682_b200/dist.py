@@ -9,6 +9,10 @@ per-point binned spectra and chi^2 (BASELINE.json north_star), done with NCCL
 all_gather_into_tensor over NVLink, chunk-pipelined on a communication stream so
 that chunk c's gather overlaps chunk c+1's kernel.
 
+End to end (host buffers in and out), NodeSharedHost + oscprob_batch_host_sharded
+gather the result into host memory shared by the node's ranks, each GPU writing its
+own rows over its own PCIe link.
+
 One point's arithmetic never depends on the other points in a call, so the
 gathered result is bitwise identical for every G (tests/test_dist_gloo.py on CPU
 with gloo; tests/test_gpu_parity.py split invariance on the GPU).
@@ -217,3 +221,76 @@ class FusedGather:
     def result(self):
         """The gathered (spectra, chi2) as local tensors (all ranks with multicast, rank 0 else)."""
         return self.spectra, self.chi2
+
+
+class NodeSharedHost:
+    """Host output arrays shared by the ranks of one node (POSIX shared memory) and
+    page-locked in every rank's CUDA context, for the end-to-end multi-GPU step: each rank's
+    host-buffer batch call writes its own rows of the spectra and chi^2 straight from its GPU
+    over its own PCIe link, so after a barrier the node's host memory holds the whole,
+    gathered result (end to end including the gather; the paper's
+    transfer-inclusive timing).  Rank 0 creates the segment; the name travels
+    through the process group's store.
+
+    arrays: dict name -> numpy float64 array of the requested shape (same memory on all
+    ranks).  close() unpins and detaches (rank 0 also unlinks, after a barrier).
+    """
+
+    def __init__(self, shapes: dict, rank: int, store, tag: str = "gna_node_shared",
+                 pin: bool = True):
+        from multiprocessing import shared_memory
+        self.rank = rank
+        sizes = {k: int(np.prod(s)) * 8 for k, s in shapes.items()}
+        offs, total = {}, 0
+        for k, n in sizes.items():
+            offs[k] = total
+            total += -(-n // 4096) * 4096  # page-aligned arrays
+        self.nbytes = max(total, 4096)
+        if rank == 0:
+            self.shm = shared_memory.SharedMemory(create=True, size=self.nbytes)
+            store.set(tag, self.shm.name)
+        else:
+            store.wait([tag])
+            self.shm = shared_memory.SharedMemory(name=store.get(tag).decode())
+            try:  # the creator owns the segment's lifetime (Python 3.12 tracks attaches too)
+                from multiprocessing import resource_tracker
+                resource_tracker.unregister(self.shm._name, "shared_memory")
+            except Exception:  # noqa: BLE001
+                pass
+        self.arrays = {k: np.ndarray(s, dtype=np.float64, buffer=self.shm.buf, offset=offs[k])
+                       for k, s in shapes.items()}
+        self.pinned = False
+        if pin:
+            import torch
+            addr = np.frombuffer(self.shm.buf, dtype=np.uint8).ctypes.data
+            rc = torch.cuda.cudart().cudaHostRegister(addr, self.nbytes, 0)
+            if int(rc) != 0:
+                raise RuntimeError("cudaHostRegister of the node-shared buffer failed (%s)" % rc)
+            self._addr, self.pinned = addr, True
+
+    def close(self, barrier=None):
+        if self.pinned:
+            import torch
+            torch.cuda.cudart().cudaHostUnregister(self._addr)
+            self.pinned = False
+        self.arrays = {}
+        if barrier is not None:
+            barrier()
+        self.shm.close()
+        if self.rank == 0:
+            self.shm.unlink()
+
+
+def oscprob_batch_host_sharded(sb: ShardedBatch, points: dict, L_km, omega, edges, order: int,
+                               data, out: NodeSharedHost, barrier: Callable, spectra=True):
+    """End-to-end multi-GPU batch over HOST arrays: rank r runs the host-buffer batch
+    (gna_oscprob_batch_host: chunked H2D -> kernels -> D2H on three streams) on its points
+    [lo, hi), writing rows [lo, hi) of the node-shared spectra / chi2, then all ranks meet at
+    `barrier`; afterwards every rank sees the full result in host memory.  `points` holds the
+    rank's own points (host float64 arrays of hi - lo values, pinned for full PCIe speed)."""
+    from . import oscprob_batch_host
+    if sb.count > 0:
+        oscprob_batch_host(points, L_km, omega, edges, order, data=data,
+                           spectra=out.arrays["spectra"][sb.lo:sb.hi] if spectra else False,
+                           chi2=out.arrays["chi2"][sb.lo:sb.hi])
+    barrier()

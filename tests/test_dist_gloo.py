@@ -190,3 +190,39 @@ def test_auto_chunks():
     assert bench.auto_chunks(1000, 1, per_point) == 1
     assert [bench.auto_chunks(1000, g, per_point) for g in (2, 4, 8)] == [4, 2, 1]
     assert bench.auto_chunks(10_000, 8, 10_000) == 1  # cfg4
+
+
+def _shared_worker(rank, world, port, P, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        store = dist.distributed_c10d._get_default_store()
+        nb = 5
+        out = gdist.NodeSharedHost({"spectra": (P, nb), "chi2": (P,)}, rank, store, pin=False)
+        sb = gdist.ShardedBatch(P, nb, world, rank)
+        # each rank writes only its own rows (what gna_oscprob_batch_host does on the GPU)
+        out.arrays["spectra"][sb.lo:sb.hi] = np.arange(sb.lo, sb.hi)[:, None] + np.arange(nb) / 10
+        out.arrays["chi2"][sb.lo:sb.hi] = -np.arange(sb.lo, sb.hi, dtype=float)
+        dist.barrier()
+        out_q.put((rank, out.arrays["spectra"].copy(), out.arrays["chi2"].copy()))
+        out.close(barrier=dist.barrier)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,P", [(2, 11), (3, 7)])
+def test_node_shared_host_gathers_every_ranks_rows(world, P):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shared_worker, args=(r, world, port, P, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.arange(P)[:, None] + np.arange(5) / 10
+    for rank, s, x in res:
+        assert np.array_equal(s, want) and np.array_equal(x, -np.arange(P, dtype=float)), rank

@@ -47,6 +47,10 @@ VARIANTS = {
     "gl_split_bw2": dict(GNA_GL_SPLIT_BW=2, GNA_GL_SPLIT_MINB=4),
     "gl_split_mb21": dict(GNA_GL_SPLIT_MINB=21),
     "gl_split_mb16": dict(GNA_GL_SPLIT_MINB=16),
+    "scan_a8": dict(GNA_SCAN_A=8),
+    "scan_a16": dict(GNA_SCAN_A=16),
+    "scan_a8_t256": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=256),
+    "scan_a16_t256": dict(GNA_SCAN_A=16, GNA_SCAN_THREADS=256),
     "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
     "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
     "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
@@ -57,7 +61,7 @@ KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb
            r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
            r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E",
            r"k_oscprob_batchILi1ELi10ELi0ELb1E", r"k_gl_integrate_splitILi10EN3gna7PeeCoef",
-           r"k_gl_integrate_tbILi10EN3gna7PeeCoef"]
+           r"k_gl_integrate_tbILi10EN3gna7PeeCoef", r"k_scan_expand"]
 
 
 def main(names):
