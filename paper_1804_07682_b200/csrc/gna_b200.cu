@@ -442,13 +442,24 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   const int64_t nchunk = (g->nmix + kScanA - 1) / kScanA;
   const int64_t nblk = g->nmass * nchunk;
   if ((nsetup + 127) / 128 > 0x7fffffffLL || nblk > 0x7fffffffLL) return GNA_EINVAL;
-  k_scan_setup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
+  // node groups of 5 (4, 3) when they divide the order, else 4 with a ragged last group
+  auto ksetup = (order % 5 == 0)   ? k_scan_setup<5>
+                : (order % 4 == 0) ? k_scan_setup<4>
+                : (order % 3 == 0) ? k_scan_setup<3>
+                                   : k_scan_setup<GNA_SCAN_G_DEFAULT>;
+  ksetup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
       a, g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges, chi2 ? data : nullptr, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
-  k_scan_expand<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
-                                                        chi2 ? data : nullptr, chi2);
+  const bool vec2 = (nbins & 1) == 0 && ((uintptr_t)spectra & 15) == 0 &&
+                    (!chi2 || ((uintptr_t)data & 15) == 0);
+  if (GNA_SCAN_EXPAND2 && vec2)
+    k_scan_expand2<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
+                                                           chi2 ? data : nullptr, chi2);
+  else
+    k_scan_expand<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
+                                                          chi2 ? data : nullptr, chi2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);

@@ -57,6 +57,14 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
 // reciprocal and run as three independent sin^2 chains (two nodes per iteration:
 // six chains) -> G[c][*][k]; threads with c == 0 also write H[k] and 1/D[k]; extra
 // threads compute the mixing weights of each mixing point.
+#ifndef GNA_SCAN_G_DEFAULT
+#define GNA_SCAN_G_DEFAULT 4
+#endif
+// Nodes are taken kG at a time: the kG reciprocals and the 3 x kG sin^2 terms of a group are
+// independent chains (ILP 3 kG; round 1's scalar loop ran ~2 chains and was latency-bound:
+// 9.5 us for ~2.3 us of FP64 work, profiles/r02_ncu_scan_summary.txt); each term is then
+// folded over the group's nodes in ascending order with the same FMAs, so G is unchanged.
+template <int kG>
 __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
                                                     const double* __restrict__ th13,
                                                     const double* __restrict__ d21,
@@ -82,13 +90,25 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
       const double k1 = phase_slope(m31, a.L[b]);
       const double k2 = phase_slope(m32, a.L[b]);
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll 2
-      for (int i = 0; i < a.order; ++i) {
-        const double invE = gna::rcp(fma(h, c_gl_t[off + i], ctr));
-        const double wi = c_gl_w[off + i];
-        s0 = fma(wi, gna::sin2c(k0, invE), s0);
-        s1 = fma(wi, gna::sin2c(k1, invE), s1);
-        s2 = fma(wi, gna::sin2c(k2, invE), s2);
+      for (int i0 = 0; i0 < a.order; i0 += kG) {
+        const int n = a.order - i0 < kG ? a.order - i0 : kG;
+        double v0[kG], v1[kG], v2[kG];
+#pragma unroll
+        for (int i = 0; i < kG; ++i) {
+          const double invE = gna::rcp(fma(h, c_gl_t[off + i0 + (i < n ? i : 0)], ctr));
+          v0[i] = gna::sin2c(k0, invE);
+          v1[i] = gna::sin2c(k1, invE);
+          v2[i] = gna::sin2c(k2, invE);
+        }
+#pragma unroll
+        for (int i = 0; i < kG; ++i) {
+          if (i < n) {
+            const double wi = c_gl_w[off + i0 + i];
+            s0 = fma(wi, v0[i], s0);
+            s1 = fma(wi, v1[i], s1);
+            s2 = fma(wi, v2[i], s2);
+          }
+        }
       }
       // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
       const double ob = a.omega[b] * h;
@@ -180,6 +200,88 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
 #endif
         const double d = T - D;
         x2[j] = fma(d * d, iD, x2[j]);
+      }
+    }
+    G0 = nG0, G1 = nG1, G2 = nG2, H = nH, D = nD, iD = niD;
+  }
+  if (chi2) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < kScanA; ++j) {
+      double v = x2[j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) s_x2[j][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < na) {
+      double t = 0.0;
+#pragma unroll
+      for (int i = 0; i < kScanThreads / 32; ++i) t += s_x2[threadIdx.x][i];
+      chi2[c * nmix + a0 + threadIdx.x] = t;
+    }
+  }
+}
+
+// Stage B for even nbins and 16-byte aligned outputs (GNA_SCAN_EXPAND2, default):
+// k_scan_expand with each thread on two adjacent bins (16-byte loads and stores: half the
+// memory instructions and loop trips, twice the bytes in flight per load; cfg4grid
+// 30.7 -> 28.6 us per step, expand 23 -> 20 us under ncu).  T is the same expression per bin,
+// so the spectra are bitwise unchanged; a lane's chi^2 terms are accumulated pair by pair.
+#ifndef GNA_SCAN_EXPAND2
+#define GNA_SCAN_EXPAND2 1
+#endif
+__global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int64_t nbins,
+                                                               int64_t nchunk, ScanWs w,
+                                                               double* __restrict__ spectra,
+                                                               const double* __restrict__ data,
+                                                               double* __restrict__ chi2) {
+  __shared__ double s_x2[kScanA][kScanThreads / 32];
+  const int64_t c = blockIdx.x / nchunk;
+  const int64_t a0 = (blockIdx.x - c * nchunk) * kScanA;
+  const int na = (int)min((int64_t)kScanA, nmix - a0);
+  double w0[kScanA], w1[kScanA], w2[kScanA], x2[kScanA];
+#pragma unroll
+  for (int j = 0; j < kScanA; ++j) {
+    const int64_t aj = a0 + (j < na ? j : 0);
+    const double4 wm = *reinterpret_cast<const double4*>(w.wmix + 4 * aj);
+    w0[j] = wm.x;
+    w1[j] = wm.y;
+    w2[j] = wm.z;
+    x2[j] = 0.0;
+  }
+  const int64_t np = nbins >> 1;
+  const double2* __restrict__ g0 = reinterpret_cast<const double2*>(w.G + (c * 3) * nbins);
+  const double2* __restrict__ g1 = g0 + np;
+  const double2* __restrict__ g2 = g1 + np;
+  const double2* __restrict__ Hv = reinterpret_cast<const double2*>(w.H);
+  const double2* __restrict__ Dv = reinterpret_cast<const double2*>(data);
+  const double2* __restrict__ iDv = reinterpret_cast<const double2*>(w.invD);
+  double2* __restrict__ out =
+      spectra ? reinterpret_cast<double2*>(spectra + (c * nmix + a0) * nbins) : nullptr;
+  int64_t q = threadIdx.x;
+  double2 G0 = {0, 0}, G1 = {0, 0}, G2 = {0, 0}, H = {0, 0}, D = {0, 0}, iD = {0, 0};
+  if (q < np) {
+    G0 = g0[q], G1 = g1[q], G2 = g2[q], H = Hv[q];
+    if (chi2) D = Dv[q], iD = iDv[q];
+  }
+  for (; q < np; q += kScanThreads) {
+    const int64_t qn = q + kScanThreads;
+    double2 nG0 = {0, 0}, nG1 = {0, 0}, nG2 = {0, 0}, nH = {0, 0}, nD = {0, 0}, niD = {0, 0};
+    if (qn < np) {
+      nG0 = g0[qn], nG1 = g1[qn], nG2 = g2[qn], nH = Hv[qn];
+      if (chi2) nD = Dv[qn], niD = iDv[qn];
+    }
+#pragma unroll
+    for (int j = 0; j < kScanA; ++j) {
+      if (j < na) {
+        double2 T;
+        T.x = H.x - fma(w0[j], G0.x, fma(w1[j], G1.x, w2[j] * G2.x));
+        T.y = H.y - fma(w0[j], G0.y, fma(w1[j], G1.y, w2[j] * G2.y));
+        if (out) out[j * np + q] = T;
+        const double dx = T.x - D.x, dy = T.y - D.y;
+        x2[j] = fma(dx * dx, iD.x, x2[j]);
+        x2[j] = fma(dy * dy, iD.y, x2[j]);
       }
     }
     G0 = nG0, G1 = nG1, G2 = nG2, H = nH, D = nD, iD = niD;

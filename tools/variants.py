@@ -51,6 +51,11 @@ VARIANTS = {
     "scan_a16": dict(GNA_SCAN_A=16),
     "scan_a8_t256": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=256),
     "scan_a16_t256": dict(GNA_SCAN_A=16, GNA_SCAN_THREADS=256),
+    "scan_a5": dict(GNA_SCAN_A=5),
+    "scan_a2": dict(GNA_SCAN_A=2),
+    "scan_a3": dict(GNA_SCAN_A=3),
+    "scan_t64": dict(GNA_SCAN_THREADS=64),
+    "scan_noexp2": dict(GNA_SCAN_EXPAND2=0),
     "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
     "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
     "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
