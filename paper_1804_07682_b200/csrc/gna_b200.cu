@@ -243,6 +243,9 @@ cudaError_t launch_pdl_single(void (*kern)(KArgs...), unsigned grid, unsigned bl
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+#ifndef GNA_BATCH_PT_BPSM
+#define GNA_BATCH_PT_BPSM 0
+#endif
 // launch of the batch kernels on already-validated device arguments
 template <int kOut, bool kMixed>
 int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double* omega,
@@ -330,7 +333,14 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
       kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed> : k_oscprob_batch_pt<10, 6, kOut, kMixed>;
 #endif
     const int64_t ng = (pts->npoints + 31) / 32;
-    const size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);
+    size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);
+#if GNA_BATCH_PT_BPSM
+    // wave shaping (experiment): pad shared memory so that at most GNA_BATCH_PT_BPSM one-warp
+    // blocks fit on an SM (228 KiB per SM, 1 KiB reserved per block)
+    smem_pt = std::max<size_t>(smem_pt, (size_t)233472 / GNA_BATCH_PT_BPSM - 1024);
+    if (smem_pt > 48 * 1024)
+      cudaFuncSetAttribute(kpt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pt);
+#endif
     pt_sub = GNA_BATCH_PT_SUB;
     const int lv = pt_sub == 4 ? 3 : pt_sub == 2 ? 4 : 5;
     if (ng * bpp * pt_sub > 0x7fffffffLL) return GNA_EINVAL;

@@ -51,6 +51,13 @@ VARIANTS = {
     "scan_a16": dict(GNA_SCAN_A=16),
     "scan_a8_t256": dict(GNA_SCAN_A=8, GNA_SCAN_THREADS=256),
     "scan_a16_t256": dict(GNA_SCAN_A=16, GNA_SCAN_THREADS=256),
+    "pt_b23_s1": dict(GNA_BATCH_PT_BPSM=23, GNA_BATCH_PT_SUB=1),
+    "pt_b23_s2": dict(GNA_BATCH_PT_BPSM=23, GNA_BATCH_PT_SUB=2),
+    "pt_b24_s4": dict(GNA_BATCH_PT_BPSM=24, GNA_BATCH_PT_SUB=4),
+    "pt_s1": dict(GNA_BATCH_PT_SUB=1),
+    "pt_s4": dict(GNA_BATCH_PT_SUB=4),
+    "gl_split_bw4": dict(GNA_GL_SPLIT_BW=4, GNA_GL_SPLIT_MINB=2),
+    "gl_split_bw2_mb5": dict(GNA_GL_SPLIT_BW=2, GNA_GL_SPLIT_MINB=5),
     "scan_a5": dict(GNA_SCAN_A=5),
     "scan_a2": dict(GNA_SCAN_A=2),
     "scan_a3": dict(GNA_SCAN_A=3),
@@ -66,7 +73,7 @@ KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb
            r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
            r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E",
            r"k_oscprob_batchILi1ELi10ELi0ELb1E", r"k_gl_integrate_splitILi10EN3gna7PeeCoef",
-           r"k_gl_integrate_tbILi10EN3gna7PeeCoef", r"k_scan_expand"]
+           r"k_gl_integrate_tbILi10EN3gna7PeeCoef", r"k_scan_expand", r"k_oscprob_batch_ptILi5ELi3ELi0ELb0E"]
 
 
 def main(names):
