@@ -375,12 +375,14 @@ def _cpu_model():
 
 
 def auto_chunks(npoints: int, world: int, evals_per_point: int) -> int:
-    """Gather pipeline depth for N > 1: one chunk per ~1e8 energy points of
-    the rank's shard (>= ~0.25 ms of kernel, i.e. many waves per chunk), 1 to 4 chunks."""
+    """Gather pipeline depth for N > 1: up to 4 chunks, each >= ~2.5e7 energy
+    points of the rank's shard (>= ~60 us of kernel, several waves), so that all but the last
+    chunk's all-gather hides under the next chunk's kernel; chunks after the first reuse the
+    node tables (GNA_WS_TABLES_VALID), so a chunk costs only its own points."""
     if world == 1:
         return 1
     per_rank = -(-npoints // world) * evals_per_point
-    return int(max(1, min(4, round(per_rank / 1e8))))
+    return int(max(1, min(4, round(per_rank / 2.5e7))))
 
 
 def _free_port() -> int:

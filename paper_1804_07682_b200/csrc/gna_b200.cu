@@ -17,6 +17,7 @@
 #include <complex>
 #include <utility>
 #include <mutex>
+#include <vector>
 
 #include "../../include/gna_b200.h"
 #include "gna_common.cuh"
@@ -617,6 +618,15 @@ int run_pipeline(Staging* S, cudaStream_t caller, int64_t nchunks, FH h2d, FK ke
     return code;
   };
   if ((e = cudaEventRecord(S->ev_in, caller)) != cudaSuccess) return cuda_fail(e);
+  if (nchunks == 1) {
+    // nothing to overlap: the three stages in order on one stream, no cross-stream events
+    // (small calls — cfg1/cfg2-sized single points, the chi^2-only fit step — are latency-bound)
+    cudaStream_t s1 = S->st[1];
+    if ((e = cudaStreamWaitEvent(s1, S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
+    if ((rc = h2d(0, 0, s1)) || (rc = kern(0, 0, s1)) || (rc = d2h(0, 0, s1))) return fail(rc);
+    if ((e = cudaStreamSynchronize(s1)) != cudaSuccess) return fail(cuda_fail(e));
+    return GNA_OK;
+  }
   for (int i = 0; i < 3; ++i)
     if ((e = cudaStreamWaitEvent(S->st[i], S->ev_in, 0)) != cudaSuccess) return cuda_fail(e);
   for (int64_t ci = 0; ci < nchunks; ++ci) {
@@ -646,6 +656,42 @@ int h2d_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 int d2h_copy(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
+}
+
+// Chunk boundaries over [0, total) for run_pipeline: chunks of `chunk` units, the first
+// and / or last ones tapered (chunk/8, chunk/4, chunk/2) so that the pipeline's unhidden
+// head (the first H2D) and tail (the last D2H) are short.  Sizes are multiples of `align`
+// (except a ragged end) and never exceed `chunk`.  Returns the nchunks + 1 offsets.
+std::vector<int64_t> plan_chunks(int64_t total, int64_t chunk, bool taper_head, bool taper_tail,
+                                 int64_t align) {
+  std::vector<int64_t> sizes, tail;
+  auto al = [&](int64_t v) { return std::max<int64_t>(align, v / align * align); };
+  int64_t rem = total;
+  const int64_t tapered = (taper_head ? chunk - chunk / 8 : 0) + (taper_tail ? chunk - chunk / 8 : 0);
+  if (total > 2 * chunk + tapered && chunk >= 8 * align) {
+    if (taper_head)
+      for (int64_t c = chunk / 8; c < chunk; c *= 2) {
+        sizes.push_back(al(c));
+        rem -= sizes.back();
+      }
+    if (taper_tail)
+      for (int64_t c = chunk / 8; c < chunk; c *= 2) {
+        tail.push_back(al(c));
+        rem -= tail.back();
+      }
+  }
+  const int64_t nmid = (rem + chunk - 1) / chunk;
+  if (nmid > 0) {  // nmid near-equal chunks (<= chunk each; the last one takes the rest)
+    int64_t msz = (rem + nmid - 1) / nmid;
+    msz = std::min<int64_t>(chunk, (msz + align - 1) / align * align);
+    for (int64_t i = 0; i + 1 < nmid; ++i) sizes.push_back(msz);
+    sizes.push_back(rem - (nmid - 1) * msz);
+  }
+  for (auto it = tail.rbegin(); it != tail.rend(); ++it) sizes.push_back(*it);
+  std::vector<int64_t> off(1, 0);
+  for (int64_t m : sizes)
+    if (m > 0) off.push_back(off.back() + m);
+  return off;
 }
 
 }  // namespace
@@ -747,18 +793,18 @@ int gna_gl_integrate_host(const gna_osc_params* p, double L_km, const double* h_
   double* base = (double*)S->buf;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  const int64_t nchunks = (nbins + chunk - 1) / chunk;
-  auto rows = [&](int64_t ci) { return std::min<int64_t>(chunk, nbins - ci * chunk); };
+  const std::vector<int64_t> off = plan_chunks(nbins, chunk, true, true, 1);
+  auto rows = [&](int64_t ci) { return off[ci + 1] - off[ci]; };
   return run_pipeline(
-      S, (cudaStream_t)stream, nchunks,
+      S, (cudaStream_t)stream, (int64_t)off.size() - 1,
       [&](int64_t ci, int r, cudaStream_t s) {
-        return h2d_copy(base + r * slot, h_edges + ci * chunk, (size_t)(rows(ci) + 1) * 8, s);
+        return h2d_copy(base + r * slot, h_edges + off[ci], (size_t)(rows(ci) + 1) * 8, s);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
         return launch_gl(c, base + r * slot, rows(ci), order, base + r * slot + chunk + 2, s);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
-        return d2h_copy(h_bins + ci * chunk, base + r * slot + chunk + 2, (size_t)rows(ci) * 8, s);
+        return d2h_copy(h_bins + off[ci], base + r * slot + chunk + 2, (size_t)rows(ci) * 8, s);
       });
 }
 
@@ -961,18 +1007,18 @@ int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_
   double* base = (double*)S->buf;
   PeeCoef c;
   make_coef(p, L_km, &c);
-  const int64_t nchunks = (n + chunk - 1) / chunk;
-  auto len = [&](int64_t ci) { return std::min<int64_t>(chunk, n - ci * chunk); };
+  const std::vector<int64_t> off = plan_chunks(n, chunk, true, true, 2);
+  auto len = [&](int64_t ci) { return off[ci + 1] - off[ci]; };
   return run_pipeline(
-      S, (cudaStream_t)stream, nchunks,
+      S, (cudaStream_t)stream, (int64_t)off.size() - 1,
       [&](int64_t ci, int r, cudaStream_t s) {
-        return h2d_copy(base + r * slot, h_E + ci * chunk, (size_t)len(ci) * 8, s);
+        return h2d_copy(base + r * slot, h_E + off[ci], (size_t)len(ci) * 8, s);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
         return launch_eval(c, base + r * slot, len(ci), base + r * slot + chunk, s);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
-        return d2h_copy(h_P + ci * chunk, base + r * slot + chunk, (size_t)len(ci) * 8, s);
+        return d2h_copy(h_P + off[ci], base + r * slot + chunk, (size_t)len(ci) * 8, s);
       });
 }
 
@@ -1023,10 +1069,11 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   q += b_ws;
   char* d_slots = q;
   const double* hsrc[4] = {h_pts->theta12, h_pts->theta13, h_pts->dm2_21, h_pts->dm2_31};
-  const int64_t nchunks = (P + chunk_points - 1) / chunk_points;
-  auto rows = [&](int64_t ci) { return std::min<int64_t>(chunk_points, P - ci * chunk_points); };
+  // tapered tail: the last D2H of spectra (not hidden by any kernel) stays short
+  const std::vector<int64_t> off = plan_chunks(P, chunk_points, false, h_spectra != nullptr, 1);
+  auto rows = [&](int64_t ci) { return off[ci + 1] - off[ci]; };
   return run_pipeline(
-      S, (cudaStream_t)stream, nchunks,
+      S, (cudaStream_t)stream, (int64_t)off.size() - 1,
       [&](int64_t ci, int, cudaStream_t s) {
         if (ci > 0) return (int)GNA_OK;  // every input goes up with the first chunk
         int r2 = h2d_copy(d_edges, h_edges, (size_t)(nbins + 1) * 8, s);
@@ -1037,7 +1084,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
       [&](int64_t ci, int r, cudaStream_t s) {
         int r2 = GNA_OK;
         if (ci == 0 && (r2 = launch_batch_tables(d_edges, nbins, order, d_tables, s))) return r2;
-        const int64_t o = ci * chunk_points, m = rows(ci);
+        const int64_t o = off[ci], m = rows(ci);
         const gna_param_batch dp = {d_pts + o, d_pts + P + o, d_pts + 2 * P + o,
                                     d_pts + 3 * P + o, m};
         return launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order,
@@ -1045,7 +1092,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
                             d_chi ? d_chi + o : nullptr, d_ws, s, kOutLocal, false, d_tables);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
-        const int64_t o = ci * chunk_points, m = rows(ci);
+        const int64_t o = off[ci], m = rows(ci);
         int r2 = GNA_OK;
         if (h_spectra)
           r2 = d2h_copy(h_spectra + o * nbins, d_slots + r * b_slot, (size_t)m * nbins * 8, s);

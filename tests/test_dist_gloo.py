@@ -188,8 +188,8 @@ def test_auto_chunks():
     import bench
     per_point = 8 * 10_000 * 10  # cfg5
     assert bench.auto_chunks(1000, 1, per_point) == 1
-    assert [bench.auto_chunks(1000, g, per_point) for g in (2, 4, 8)] == [4, 2, 1]
-    assert bench.auto_chunks(10_000, 8, 10_000) == 1  # cfg4
+    assert [bench.auto_chunks(1000, g, per_point) for g in (2, 4, 8)] == [4, 4, 4]
+    assert [bench.auto_chunks(10_000, g, 10_000) for g in (2, 4, 8)] == [2, 1, 1]  # cfg4
 
 
 def _shared_worker(rank, world, port, P, out_q):

@@ -36,8 +36,9 @@ CAPTURES = {
     "batch_pt_mixed": ("cfg4_mixed", "k_oscprob_batch_pt<..., kMixed>"),
     "eval": ("cfg3", "k_oscprob_eval_tma"),
     "eval_ab": ("cfg3emu", "k_oscprob_eval_tma<PabCoef>"),
-    "gl": ("cfg2", "k_gl_integrate"),
-    "scan": ("cfg4grid", "k_scan_expand"),
+    "gl": ("cfg2", "k_gl_integrate_split"),
+    "scan": ("cfg4grid", "k_scan_expand2"),
+    "scan_setup": ("cfg4grid_setup", "k_scan_setup"),
     "batch_mixed": ("cfg5_mixed", "k_oscprob_batch<..., kMixed>"),
 }
 
@@ -126,6 +127,8 @@ def main():
                 fp / n, n)
         with open(os.path.join(prof, "%s_final_ncu_%s_summary.txt" % (R, name)), "w") as f:
             f.write(text)
+        if w.endswith("_setup"):  # secondary kernel of a workload: summary only
+            continue
         rd = float(kv.get("dram__bytes_read.sum", "0") or 0)
         wr = float(kv.get("dram__bytes_write.sum", "0") or 0)
         unit_r = text.split("dram__bytes_read.sum\t")[1].split("\n")[0].split("\t")[-1]
@@ -157,6 +160,10 @@ def main():
             v = float(r[i_v].replace(",", "")) * to_us.get(r[i_u], 1.0)
             n, t = agg.get(r[i_k], (0, 0.0))
             agg[r[i_k]] = (n + 1, t + v)
+        # the live FP64 probe (build/probe_fp64, run by bench.py before its timed region) is
+        # listed apart: it is neither the product nor part of a step
+        probe = {k: v for k, v in agg.items() if k.startswith("k_dfma")}
+        agg = {k: v for k, v in agg.items() if not k.startswith("k_dfma")}
         total = sum(t for _, t in agg.values()) or 1.0
         with open(os.path.join(prof, "%s_launches_default_cfg5_summary.txt" % R), "w") as f:
             f.write("# ncu launch list of `python bench.py --steps 20 --warmup 3` (default cfg5 "
@@ -165,6 +172,9 @@ def main():
                     "not absolutes\n")
             for k, (n, t) in sorted(agg.items(), key=lambda z: -z[1][1]):
                 f.write("%-60.60s n=%4d avg=%9.2fus share=%.3f\n" % (k, n, t / n, t / total))
+            for k, (n, t) in probe.items():
+                f.write("# not in the shares: %s n=%d avg=%.2fus (bench.py's FP64 peak probe, "
+                        "before the timed region)\n" % (k[:40], n, t / n))
         print("launches", len(rows) - 1)
 
 

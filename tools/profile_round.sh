@@ -33,5 +33,6 @@ prof batch_pt_mixed cfg4 k_oscprob_batch_pt "--precision mixed"
 prof eval cfg3 k_oscprob_eval_tma
 prof eval_ab cfg3emu k_oscprob_eval_tma
 prof gl cfg2 k_gl_integrate
-prof scan cfg4grid k_scan
+prof scan cfg4grid k_scan_expand
+prof scan_setup cfg4grid k_scan_setup
 prof batch_mixed cfg5 '^k_oscprob_batch$' "--precision mixed"
