@@ -552,6 +552,9 @@ int launch_eval(const Coef& c, const double* E, int64_t n, double* P, cudaStream
 // c+2's H2D run at the same time (the paper's "CUDA Streams ... overlapped execution,
 // asynchronous memory copying") while every kernel still gets the whole GPU.
 constexpr int kRing = 3;
+#ifndef GNA_HOST_SPECTRA_MAX
+#define GNA_HOST_SPECTRA_MAX (1ull << 31)  // device bytes for un-ringed batch spectra staging
+#endif
 struct Staging {
   bool init = false;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
@@ -609,8 +612,13 @@ int stage_init(Staging* S) {
 // after the kernel of chunk ci - kRing has read it, and its output only after the D2H of
 // chunk ci - kRing has copied it out.  Waits for the caller's stream first; returns after
 // all three streams are idle (also on error, so no copy outlives the call).
+//   h2d_each = false: only chunk 0 has an H2D stage (the batch uploads everything at once), so
+//     later kernels do not wait on the H2D stream;
+//   out_ring = false: each chunk writes its own output region (no slot reuse), so the compute
+//     stream never waits on the D2H stream and the kernels run back to back.
 template <class FH, class FK, class FD>
-int run_pipeline(Staging* S, cudaStream_t caller, int64_t nchunks, FH h2d, FK kern, FD d2h) {
+int run_pipeline(Staging* S, cudaStream_t caller, int64_t nchunks, FH h2d, FK kern, FD d2h,
+                 bool h2d_each = true, bool out_ring = true) {
   cudaError_t e = cudaSuccess;
   int rc = GNA_OK;
   auto fail = [&](int code) {
@@ -632,11 +640,14 @@ int run_pipeline(Staging* S, cudaStream_t caller, int64_t nchunks, FH h2d, FK ke
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     const int r = (int)(ci % kRing);
     const bool reuse = ci >= kRing;
-    if (reuse && (e = cudaStreamWaitEvent(S->st[0], S->ev_k[r], 0)) != cudaSuccess) break;
-    if ((rc = h2d(ci, r, S->st[0]))) return fail(rc);
-    if ((e = cudaEventRecord(S->ev_h[r], S->st[0])) != cudaSuccess) break;
-    if ((e = cudaStreamWaitEvent(S->st[1], S->ev_h[r], 0)) != cudaSuccess) break;
-    if (reuse && (e = cudaStreamWaitEvent(S->st[1], S->ev_d[r], 0)) != cudaSuccess) break;
+    if (h2d_each || ci == 0) {
+      if (reuse && (e = cudaStreamWaitEvent(S->st[0], S->ev_k[r], 0)) != cudaSuccess) break;
+      if ((rc = h2d(ci, r, S->st[0]))) return fail(rc);
+      if ((e = cudaEventRecord(S->ev_h[r], S->st[0])) != cudaSuccess) break;
+      if ((e = cudaStreamWaitEvent(S->st[1], S->ev_h[r], 0)) != cudaSuccess) break;
+    }
+    if (out_ring && reuse && (e = cudaStreamWaitEvent(S->st[1], S->ev_d[r], 0)) != cudaSuccess)
+      break;
     if ((rc = kern(ci, r, S->st[1]))) return fail(rc);
     if ((e = cudaEventRecord(S->ev_k[r], S->st[1])) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(S->st[2], S->ev_k[r], 0)) != cudaSuccess) break;
@@ -1051,8 +1062,13 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   const size_t b_pts = align16((size_t)4 * P * 8);
   const size_t b_chi = h_chi2 ? align16((size_t)P * 8) : 0;
   const size_t b_ws = batch_ws_bytes(chunk_points, nbase, nbins, order, h_chi2 != nullptr);
+  // spectra: one region per point (no reuse, the kernels never wait for a copy) when all of
+  // them fit in GNA_HOST_SPECTRA_MAX bytes, else a ring of kRing chunk slots
+  const size_t b_all = align16((size_t)P * nbins * 8);
+  const bool out_ring = h_spectra && b_all > (size_t)GNA_HOST_SPECTRA_MAX;
   const size_t b_slot = h_spectra ? align16((size_t)chunk_points * nbins * 8) : 0;
-  if ((rc = ensure(&S->buf, &S->cap, tb + b_edges + b_data + b_pts + b_chi + b_ws + kRing * b_slot)))
+  const size_t b_spec = !h_spectra ? 0 : out_ring ? kRing * b_slot : b_all;
+  if ((rc = ensure(&S->buf, &S->cap, tb + b_edges + b_data + b_pts + b_chi + b_ws + b_spec)))
     return rc;
   char* q = (char*)S->buf;
   double* d_tables = (double*)q;
@@ -1087,18 +1103,24 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
         const int64_t o = off[ci], m = rows(ci);
         const gna_param_batch dp = {d_pts + o, d_pts + P + o, d_pts + 2 * P + o,
                                     d_pts + 3 * P + o, m};
-        return launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order,
-                            h_spectra ? (double*)(d_slots + r * b_slot) : nullptr, d_data,
+        double* dspec = !h_spectra ? nullptr
+                        : out_ring ? (double*)(d_slots + r * b_slot)
+                                   : (double*)d_slots + o * nbins;
+        return launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data,
                             d_chi ? d_chi + o : nullptr, d_ws, s, kOutLocal, false, d_tables);
       },
       [&](int64_t ci, int r, cudaStream_t s) {
         const int64_t o = off[ci], m = rows(ci);
         int r2 = GNA_OK;
         if (h_spectra)
-          r2 = d2h_copy(h_spectra + o * nbins, d_slots + r * b_slot, (size_t)m * nbins * 8, s);
+          r2 = d2h_copy(h_spectra + o * nbins,
+                        out_ring ? (const void*)(d_slots + r * b_slot)
+                                 : (const void*)((double*)d_slots + o * nbins),
+                        (size_t)m * nbins * 8, s);
         if (!r2 && h_chi2) r2 = d2h_copy(h_chi2 + o, d_chi + o, (size_t)m * 8, s);
         return r2;
-      });
+      },
+      /*h2d_each=*/false, out_ring);
 }
 
 void gna_release(void) {
