@@ -8,6 +8,8 @@ gpurun: python -m pytest tests -m gpu
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -976,3 +978,120 @@ def test_c_abi_example_runs(gna, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.strip().endswith("ok")
+
+
+_MC_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import torch
+from cuda.bindings import driver as d
+import paper_1804_07682_b200 as gna
+import synth
+
+
+def ck(r):
+    err, *rest = r if isinstance(r, tuple) else (r,)
+    if err != d.CUresult.CUDA_SUCCESS:
+        raise RuntimeError(str(err))
+    return rest[0] if len(rest) == 1 else rest
+
+
+torch.zeros(1, device="cuda")  # torch's primary context is current
+dev = ck(d.cuDeviceGet(0))
+if not ck(d.cuDeviceGetAttribute(d.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev)):
+    print("NO_MULTICAST")
+    sys.exit(0)
+g = synth.rng(8100)
+P, nb, order = %(P)d, 300, 10
+pts = synth.invert_ordering(g, synth.points_uniform(g, P, dict(
+    theta12=(0.5, 0.65), theta13=(0.1, 0.2), dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3))))
+L, om = np.array([52.5, 215.0, 265.0])[:%(nbase)d], np.array([1.0, 0.06, 0.04])[:%(nbase)d]
+edges = synth.uniform_edges(nb)
+data = synth.pseudo_data(g, edges, om.sum())
+need = P * nb * 8 + P * 8
+H = d.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR
+prop = d.CUmulticastObjectProp()
+prop.numDevices = 1
+prop.handleTypes = H
+prop.size = need
+gran = ck(d.cuMulticastGetGranularity(
+    prop, d.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+aprop = d.CUmemAllocationProp()
+aprop.type = d.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+aprop.location.type = d.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+aprop.location.id = 0
+aprop.requestedHandleTypes = H
+agran = ck(d.cuMemGetAllocationGranularity(
+    aprop, d.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED))
+gr = max(int(gran), int(agran))
+size = -(-need // gr) * gr
+prop.size = size
+try:
+    mc = ck(d.cuMulticastCreate(prop))
+    ck(d.cuMulticastAddDevice(mc, dev))
+except RuntimeError as exc:
+    print("NO_MULTICAST", exc)
+    sys.exit(0)
+mem = ck(d.cuMemCreate(size, aprop, 0))
+ck(d.cuMulticastBindMem(mc, 0, mem, 0, size, 0))
+acc = d.CUmemAccessDesc()
+acc.location.type = d.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+acc.location.id = 0
+acc.flags = d.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+uc = ck(d.cuMemAddressReserve(size, gr, 0, 0))
+ck(d.cuMemMap(uc, size, 0, mem, 0))
+ck(d.cuMemSetAccess(uc, size, [acc], 1))
+mva = ck(d.cuMemAddressReserve(size, gr, 0, 0))
+ck(d.cuMemMap(mva, size, 0, mc, 0))
+ck(d.cuMemSetAccess(mva, size, [acc], 1))
+ck(d.cuMemsetD8(uc, 0xff, size))  # NaN pattern: every output must be written
+f64 = dict(dtype=torch.float64, device="cuda")
+dp = {k: torch.tensor(v, **f64) for k, v in pts.items()}
+de, dd = torch.tensor(edges, **f64), torch.tensor(data, **f64)
+base = int(mva)
+gna.oscprob_batch_ex(dp, L, om, de, order, base, base + P * nb * 8, gna.GNA_OUT_MULTICAST, data=dd)
+torch.cuda.synchronize()
+out = np.empty(P * nb + P)
+ck(d.cuMemcpyDtoH(out.ctypes.data, uc, need))
+sp, x2 = out[:P * nb].reshape(P, nb), out[P * nb:]
+ref_sp, ref_x2 = gna.oscprob_batch(dp, L, om, de, order, data=dd)
+assert np.array_equal(sp, ref_sp.cpu().numpy()) and np.array_equal(x2, ref_x2.cpu().numpy())
+np.save(%(out)r, out)
+print("MULTICAST_OK")
+"""
+
+
+@pytest.mark.parametrize("P,nbase", [(5, 3), (300, 1)])
+def test_fused_epilogue_multicast_stores_single_gpu_nvls_object(gna, P, nbase, tmp_path):
+    """NEXT-4 multicast epilogue on real NVLS hardware: a one-device multicast object
+    (cuMulticastCreate + cuMulticastBindMem, driver API) mapped at a multicast VA; the batch
+    kernel's multimem.st epilogue writes through it and the bound memory, read back through
+    its unicast mapping, equals the plain batch bit for bit and the oracle on every point
+    (per-point kernel at 5 x 3 baselines; points-across-lanes kernel at 300 x 1).  Runs in a
+    subprocess so that a fault cannot poison this test process; skips where the fabric has
+    no multicast support."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outp = str(tmp_path / "mc.npy")
+    r = subprocess.run([sys.executable, "-c", _MC_SCRIPT % dict(root=root, P=P, nbase=nbase,
+                                                                 out=outp)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    if "NO_MULTICAST" in r.stdout:
+        pytest.skip("no NVLS multicast on this device: " + r.stdout.strip()[:200])
+    assert "MULTICAST_OK" in r.stdout
+    g = synth.rng(8100)
+    pts = synth.invert_ordering(g, synth.points_uniform(g, P, dict(
+        theta12=(0.5, 0.65), theta13=(0.1, 0.2), dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3))))
+    L, om = np.array([52.5, 215.0, 265.0])[:nbase], np.array([1.0, 0.06, 0.04])[:nbase]
+    edges = synth.uniform_edges(300)
+    data = synth.pseudo_data(g, edges, om.sum())
+    out = np.load(outp)
+    sp, x2 = out[:P * 300].reshape(P, 300), out[P * 300:]
+    idx = np.unique(np.r_[0, P // 2, P - 1])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, 10, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, data))
