@@ -19,6 +19,7 @@ with gloo; tests/test_gpu_parity.py split invariance on the GPU).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Callable
 
@@ -246,12 +247,31 @@ class NodeSharedHost:
             offs[k] = total
             total += -(-n // 4096) * 4096  # page-aligned arrays
         self.nbytes = max(total, 4096)
+        # Rank 0 decides and always publishes a verdict (the segment's name, or "" when it
+        # cannot create it), so no rank waits forever.  A tmpfs smaller than the segment would
+        # SIGBUS on first touch (or when pinning), so rank 0 refuses up front.
         if rank == 0:
-            self.shm = shared_memory.SharedMemory(create=True, size=self.nbytes)
+            try:
+                st = os.statvfs("/dev/shm")
+                free = st.f_bavail * st.f_frsize
+            except OSError:
+                free = 0
+            if free < self.nbytes + (64 << 20):
+                store.set(tag, "")
+                raise RuntimeError("/dev/shm has %d MB free, the node-shared buffer needs %d MB"
+                                   % (free >> 20, self.nbytes >> 20))
+            try:
+                self.shm = shared_memory.SharedMemory(create=True, size=self.nbytes)
+            except Exception:
+                store.set(tag, "")
+                raise
             store.set(tag, self.shm.name)
         else:
             store.wait([tag])
-            self.shm = shared_memory.SharedMemory(name=store.get(tag).decode())
+            name = store.get(tag).decode()
+            if not name:
+                raise RuntimeError("rank 0 could not create the node-shared buffer")
+            self.shm = shared_memory.SharedMemory(name=name)
             try:  # the creator owns the segment's lifetime (Python 3.12 tracks attaches too)
                 from multiprocessing import resource_tracker
                 resource_tracker.unregister(self.shm._name, "shared_memory")
@@ -265,6 +285,10 @@ class NodeSharedHost:
             addr = np.frombuffer(self.shm.buf, dtype=np.uint8).ctypes.data
             rc = torch.cuda.cudart().cudaHostRegister(addr, self.nbytes, 0)
             if int(rc) != 0:
+                self.arrays = {}
+                self.shm.close()
+                if rank == 0:
+                    self.shm.unlink()
                 raise RuntimeError("cudaHostRegister of the node-shared buffer failed (%s)" % rc)
             self._addr, self.pinned = addr, True
 
