@@ -64,6 +64,64 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
 // independent chains (ILP 3 kG; round 1's scalar loop ran ~2 chains and was latency-bound:
 // 9.5 us for ~2.3 us of FP64 work, profiles/r02_ncu_scan_summary.txt); each term is then
 // folded over the group's nodes in ascending order with the same FMAs, so G is unchanged.
+// G[ij] of one (mass point, bin): sum_b omega_b h sum_i w_i sin^2 Delta_ij, nodes in groups of
+// kG (the kG reciprocals and 3 kG sin^2 terms independent chains), each term folded over the
+// nodes in ascending order.
+template <int kG>
+__device__ __forceinline__ void scan_bin_G(const ScanArgs& a, double m21, double m31,
+                                           double ctr, double h, double wsum, double& G0,
+                                           double& G1, double& G2) {
+  const int off = GNA_GL_OFF(a.order);
+  const double m32 = m31 - m21;
+  G0 = 0.0, G1 = 0.0, G2 = 0.0;
+  for (int b = 0; b < a.nbase; ++b) {
+    const double k0 = phase_slope(m21, a.L[b]);
+    const double k1 = phase_slope(m31, a.L[b]);
+    const double k2 = phase_slope(m32, a.L[b]);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int i0 = 0; i0 < a.order; i0 += kG) {
+      const int n = a.order - i0 < kG ? a.order - i0 : kG;
+      double v0[kG], v1[kG], v2[kG];
+#pragma unroll
+      for (int i = 0; i < kG; ++i) {
+        const double invE = gna::rcp(fma(h, c_gl_t[off + i0 + (i < n ? i : 0)], ctr));
+        v0[i] = gna::sin2c(k0, invE);
+        v1[i] = gna::sin2c(k1, invE);
+        v2[i] = gna::sin2c(k2, invE);
+      }
+#pragma unroll
+      for (int i = 0; i < kG; ++i) {
+        if (i < n) {
+          const double wi = c_gl_w[off + i0 + i];
+          s0 = fma(wi, v0[i], s0);
+          s1 = fma(wi, v1[i], s1);
+          s2 = fma(wi, v2[i], s2);
+        }
+      }
+    }
+    // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
+    const double ob = a.omega[b] * h;
+    G0 = fma(ob, fma(0.5, wsum, s0), G0);
+    G1 = fma(ob, fma(0.5, wsum, s1), G1);
+    G2 = fma(ob, fma(0.5, wsum, s2), G2);
+  }
+}
+
+__device__ __forceinline__ double gl_wsum(int order) {
+  const int off = GNA_GL_OFF(order);
+  double wsum = 0.0;
+  for (int i = 0; i < order; ++i) wsum += c_gl_w[off + i];
+  return wsum;
+}
+
+__device__ __forceinline__ void scan_wmix(double th12, double th13, double* wm) {
+  double s12, c12, s13, c13;
+  sincos(th12, &s12, &c12);
+  sincos(th13, &s13, &c13);
+  mixing_weights(s12, c12, s13, c13, &wm[0], &wm[1], &wm[2]);
+  wm[3] = 0.0;
+}
+
 template <int kG>
 __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
                                                     const double* __restrict__ th13,
@@ -76,46 +134,12 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
   if (t < n1) {
     const int64_t c = t / a.nbins;
     const int64_t k = t - c * a.nbins;
-    const int off = GNA_GL_OFF(a.order);
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
     const double h = 0.5 * (e1 - e0);
-    double wsum = 0.0;
-    for (int i = 0; i < a.order; ++i) wsum += c_gl_w[off + i];
-    const double m21 = d21[c], m31 = d31[c];
-    const double m32 = m31 - m21;
-    double G0 = 0.0, G1 = 0.0, G2 = 0.0;
-    for (int b = 0; b < a.nbase; ++b) {
-      const double k0 = phase_slope(m21, a.L[b]);
-      const double k1 = phase_slope(m31, a.L[b]);
-      const double k2 = phase_slope(m32, a.L[b]);
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      for (int i0 = 0; i0 < a.order; i0 += kG) {
-        const int n = a.order - i0 < kG ? a.order - i0 : kG;
-        double v0[kG], v1[kG], v2[kG];
-#pragma unroll
-        for (int i = 0; i < kG; ++i) {
-          const double invE = gna::rcp(fma(h, c_gl_t[off + i0 + (i < n ? i : 0)], ctr));
-          v0[i] = gna::sin2c(k0, invE);
-          v1[i] = gna::sin2c(k1, invE);
-          v2[i] = gna::sin2c(k2, invE);
-        }
-#pragma unroll
-        for (int i = 0; i < kG; ++i) {
-          if (i < n) {
-            const double wi = c_gl_w[off + i0 + i];
-            s0 = fma(wi, v0[i], s0);
-            s1 = fma(wi, v1[i], s1);
-            s2 = fma(wi, v2[i], s2);
-          }
-        }
-      }
-      // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
-      const double ob = a.omega[b] * h;
-      G0 = fma(ob, fma(0.5, wsum, s0), G0);
-      G1 = fma(ob, fma(0.5, wsum, s1), G1);
-      G2 = fma(ob, fma(0.5, wsum, s2), G2);
-    }
+    const double wsum = gl_wsum(a.order);
+    double G0, G1, G2;
+    scan_bin_G<kG>(a, d21[c], d31[c], ctr, h, wsum, G0, G1, G2);
     double* g = w.G + (c * 3) * a.nbins + k;
     g[0] = G0;
     g[a.nbins] = G1;
@@ -126,12 +150,7 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
     }
   } else if (t < n1 + a.nmix) {
     const int64_t mm = t - n1;
-    double s12, c12, s13, c13;
-    sincos(th12[mm], &s12, &c12);
-    sincos(th13[mm], &s13, &c13);
-    double* wm = w.wmix + 4 * mm;
-    mixing_weights(s12, c12, s13, c13, &wm[0], &wm[1], &wm[2]);
-    wm[3] = 0.0;
+    scan_wmix(th12[mm], th13[mm], w.wmix + 4 * mm);
   }
 }
 
