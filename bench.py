@@ -527,14 +527,21 @@ def main():
         local = 0  # code-path test: every rank on GPU 0 (independent kernels, no device spin)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # the fused epilogue (NEXT-4): tried by default at N > 1; `--gather fused` also runs it on
+    # one GPU, writing through a one-rank symmetric-memory window (the N > 1 code path,
+    # probe and bitwise check included, on hardware that has only one GPU)
+    batch = args.workload in ("cfg4", "cfg5")
+    want_fused = batch and (args.gather == "fused" or (args.gather == "auto" and world > 1))
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if args.backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
-            if args.gather != "nccl":
-                args.gather = "nccl"  # the fused epilogue needs one GPU per rank
+            want_fused = False  # the fused epilogue needs one GPU per rank
+    elif want_fused:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % _free_port(),
+                                rank=0, world_size=1, device_id=dev)
     gna.load(args.lib)
     c = workload(args.workload)
     f64 = dict(dtype=torch.float64, device=dev)
@@ -572,14 +579,14 @@ def main():
             args.backend, len(sb.cb), "s" if len(sb.cb) > 1 else "")
         fused_fg = None
         probe = None
-        if world > 1 and args.gather in ("auto", "fused"):
+        if want_fused:
             # the fused epilogue runs here only after it has passed the same check in an
             # isolated process group under a hard timeout (a stall or a fault there cannot
             # take this run down with it)
             probe = isolated_fused_probe(args, world, rank, dist)
             if not probe["ok"]:
                 gather_mode += " (fused epilogue not used: %s)" % probe["why"]
-        if world > 1 and args.gather in ("auto", "fused") and probe["ok"]:
+        if want_fused and probe["ok"]:
             # NEXT-4: gather fused into the kernel epilogue through symmetric memory;
             # every rank must have built it before any rank runs it, and it is validated
             # bitwise against the NCCL gather before it is used
@@ -737,7 +744,8 @@ def main():
 
     # ---------------- CUDA graph of the step (the repeated-evaluation loop of a fit):
     # one graph launch per step instead of per-call host work.  NCCL steps stay eager.
-    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1)
+    fused_used = args.workload in ("cfg4", "cfg5") and fused_fg is not None
+    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and not fused_used)
     launches_per_step = None
     if use_graph:
         KernelTimer.enabled = False
@@ -884,7 +892,7 @@ def main():
         line["config"]["gather_chunks"] = len(sb.cb)
         if probe is not None:
             line["config"]["fused_probe"] = probe
-        if world > 1:
+        if world > 1 or fused_fg is not None:
             # the gathered result after the timed steps must equal a single-GPU batch of
             # all points, bit for bit (checked on rank 0, outside the timed region)
             line["config"]["gather_verified"] = _verify_gather(
@@ -923,6 +931,7 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         _barrier(dist, args, local)
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -157,3 +157,25 @@ def test_two_rank_fused_epilogue_peer_vs_oracle_and_bitwise(tmp_path):
 @needs2
 def test_two_rank_fused_epilogue_multicast_vs_oracle_and_bitwise(tmp_path):
     _run("multicast", tmp_path)
+
+
+def test_fused_probe_runs_on_one_rank():
+    """bench.py's isolated start-up check of the fused epilogue (--fused-probe) as a one-rank
+    torch.distributed.run job on this GPU: symmetric-memory window, gna_oscprob_batch_ex with
+    peer-window stores, barrier, bitwise comparison with a local batch -> FUSED_PROBE_OK.  The
+    same code runs at N > 1 before bench.py ever uses the fused path."""
+    import subprocess
+    import sys
+    if _ngpus() < 1:
+        pytest.skip("no GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    for w in ("cfg5", "cfg4"):
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                            "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+                            "--master-port", str(_free_port()), os.path.join(root, "bench.py"),
+                            "--fused-probe", "--gpus", "1", "--workload", w],
+                           capture_output=True, text=True, timeout=300, env=env, cwd=root)
+        assert r.returncode == 0, r.stderr[-3000:]
+        assert "FUSED_PROBE_OK peer-to-root" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
