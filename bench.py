@@ -839,6 +839,13 @@ def main():
     else:
         launch_units = (units_per_rank / max(calls_per_step, 1)
                         if args.workload in ("cfg4", "cfg5") else units_per_rank)
+        per_point_ops = ops_eval
+        shared21 = shared_dm2_21(c, args, units_per_rank)
+        if shared21:
+            # the points-across-lanes kernel evaluates sin^2 Delta_21 once per warp of 32
+            # points when dm2_21 (and L) is the same for all of them: the
+            # algorithmic work per energy point is 2 point-specific terms + 1/32 of the third
+            ops_eval = (deg + 5) * (2 + 1 / 32)
         achieved = launch_units * ops_eval / (kern_avg_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": peak_ops / 1e12,
                 "unit": "T fp64-ops/s", "frac": achieved * 1e12 / peak_ops, "traffic": None,
@@ -846,10 +853,16 @@ def main():
                                "count is measured: fp64_probe below)",
                 "ops_per_energy_point": ops_eval, "sin2_poly_degree": deg,
                 "kernel_ms_per_launch": kern_avg_ms,
-                # the same time on the other basis: SURVEY §8(d)'s ~50 FP64 instructions per
-                # energy point (its estimate before the 12-op sin^2 of DESIGN.md §6.1)
-                "bases": {"executed_%d_ops" % ops_eval: achieved * 1e12 / peak_ops,
+                # the same time on the other bases: every term per point (36), and SURVEY
+                # §8(d)'s ~50 FP64 instructions per energy point (its estimate before the
+                # 12-op sin^2 of DESIGN.md §6.1)
+                "bases": {"algorithmic_%g_ops" % ops_eval: achieved * 1e12 / peak_ops,
+                          "per_point_%d_ops" % per_point_ops:
+                              launch_units * per_point_ops / (kern_avg_ms * 1e-3) / peak_ops,
                           "survey_50_ops": launch_units * 50 / (kern_avg_ms * 1e-3) / peak_ops}}
+        if shared21:
+            roof["shared_dm2_21"] = ("sin^2 Delta_21 evaluated once per warp of 32 points (same "
+                                     "dm2_21 and L for every point)")
         if fp64_probe:
             roof["fp64_probe"] = fp64_probe
             roof["frac_of_probe"] = achieved * 1e3 / fp64_probe["dfma_G_per_s"]
@@ -977,6 +990,19 @@ def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
         del pts, sp, x2
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
     return bool(float(ok) == 1.0)
+
+
+def shared_dm2_21(c, args, units_per_rank) -> bool:
+    """True when the batch runs the points-across-lanes kernel (fp64, >= 256 points on the
+    rank, <= 2 baselines) and every point has the same dm2_21, so that kernel's shared
+    sin^2 Delta_21 path is taken (k_batch.cuh, GNA_BATCH_PT_SHARED21)."""
+    if args.workload not in ("cfg4", "cfg5") or args.precision != "fp64":
+        return False
+    pts = c["points"]
+    nbase = c["L_km"].size
+    per_point = nbase * (c["edges"].size - 1) * c["order"]
+    p_rank = units_per_rank // per_point
+    return bool(nbase <= 2 and p_rank >= 256 and np.all(pts["dm2_21"] == pts["dm2_21"][0]))
 
 
 def run_fp64_probe(local: int):

@@ -466,6 +466,9 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #ifndef GNA_BATCH_PT_MINB
 #define GNA_BATCH_PT_MINB 24  // <= 80 registers: 24 warps per SM
 #endif
+#ifndef GNA_BATCH_PT_SHARED21
+#define GNA_BATCH_PT_SHARED21 1  // sin^2 Delta_21 once per warp when dm2_21 and L are shared
+#endif
 #ifndef GNA_BATCH_PT_SUB
 #define GNA_BATCH_PT_SUB 2  // sub-tiles per 32-bin tile: 1, 2 or 4
 #endif
@@ -488,10 +491,18 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #define GNA_BATCH_PT_MIN_POINTS 256
 #endif
 
-template <int N, int NT, bool kMixed>
+// kShared (fp64 only): every point of the warp has the same (2,1) phase slope per baseline
+// (the same dm2_21 and L: a scan over theta13 / dm2_31 with the solar parameters fixed, as in
+// cfg4), so sin^2 Delta_21 of each (bin, node) was evaluated once per warp into sS
+// [baseline][node][32 bins] and is read instead of recomputed by all 32 point-lanes — the
+// paper's "computed only once ... re-computed only if ... modified" inside the
+// batch.  The value read is the one sin2c returns for that bin and node, so the bits are
+// unchanged.
+template <int N, int NT, bool kMixed, bool kShared = false>
 __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&cw)[NT],
                                          const float (&wf)[NT], const double* __restrict__ sE,
-                                         const double* __restrict__ sH, int b, int i, double& A) {
+                                         const double* __restrict__ sH, int b, int i, double& A,
+                                         const double* __restrict__ sS = nullptr, int order = 0) {
   double iE[N], a[N];
 #pragma unroll
   for (int n = 0; n < N; ++n) {
@@ -524,23 +535,29 @@ __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
 #pragma unroll
-      for (int n = 0; n < N; ++n) a[n] = fma(cw[j], gna::sin2c(kq[j], iE[n]), a[n]);
+      for (int n = 0; n < N; ++n) {
+        if (kShared && j % 3 == 0)
+          a[n] = fma(cw[j], sS[((j / 3) * order + i + n) * 32 + b], a[n]);
+        else
+          a[n] = fma(cw[j], gna::sin2c(kq[j], iE[n]), a[n]);
+      }
     }
   }
 #pragma unroll
   for (int n = 0; n < N; ++n) A = fma(sH[(i + n) * 32 + b], a[n], A);
 }
 
-template <int N, int NT, bool kMixed>
+template <int N, int NT, bool kMixed, bool kShared = false>
 __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const double (&cw)[NT],
                                         const float (&wf)[NT], const double* __restrict__ sE,
-                                        const double* __restrict__ sH, int b, int i, double& A) {
+                                        const double* __restrict__ sH, int b, int i, double& A,
+                                        const double* __restrict__ sS = nullptr, int order = 0) {
   if constexpr (N > 1) {
     if (r == N - 1) {
-      pt_nodes<N - 1, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
+      pt_nodes<N - 1, NT, kMixed, kShared>(kq, cw, wf, sE, sH, b, i, A, sS, order);
       return;
     }
-    pt_tail<N - 1, NT, kMixed>(r, kq, cw, wf, sE, sH, b, i, A);
+    pt_tail<N - 1, NT, kMixed, kShared>(r, kq, cw, wf, sE, sH, b, i, A, sS, order);
   }
 }
 
@@ -551,7 +568,7 @@ __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const dou
 // kMode 0: a full tile (no bounds checks); 1: bins at or past nbins are skipped; 2: every
 // bin is computed and those at or past nbins are dropped (x2 = 0 for them in both cases, as
 // in k_oscprob_batch).
-template <int kMode, int N, int NT, int kOut, bool kMixed>
+template <int kMode, int N, int NT, int kOut, bool kMixed, bool kShared = false>
 __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (&cw)[NT],
                                           const float (&wf)[NT], double c0,
                                           const double* __restrict__ sE,
@@ -560,7 +577,7 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
                                           const double* __restrict__ sD,
                                           const double* __restrict__ sID, int order, int64_t k0,
                                           int64_t nbins, double* __restrict__ out, bool pact,
-                                          int sub, int lv) {
+                                          int sub, int lv, const double* __restrict__ sS = nullptr) {
   double r[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   double x2 = 0.0;
   const int m0 = sub << lv;
@@ -571,8 +588,10 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
     if (kMode != 1 || k0 + b < nbins) {
       double A = 0.0;
       int i = 0;
-      for (; i + N <= order; i += N) pt_nodes<N, NT, kMixed>(kq, cw, wf, sE, sH, b, i, A);
-      if (i < order) pt_tail<N, NT, kMixed>(order - i, kq, cw, wf, sE, sH, b, i, A);
+      for (; i + N <= order; i += N)
+        pt_nodes<N, NT, kMixed, kShared>(kq, cw, wf, sE, sH, b, i, A, sS, order);
+      if (i < order)
+        pt_tail<N, NT, kMixed, kShared>(order - i, kq, cw, wf, sE, sH, b, i, A, sS, order);
       const double s = fma(c0, sW[b], -A);
       if (kMode != 2 || k0 + b < nbins) {
         if (out && pact) out_store<kOut>(out + k0 + b, s);
@@ -607,6 +626,7 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   double* sW = sH + order * 32;     // [32] sum_i h w_i (same order as k_oscprob_batch)
   double* sD = sW + 32;             // [32] data
   double* sID = sD + 32;            // [32] 1 / data
+  double* sS = sID + 32;            // fp64: [NT/3][order][32] shared sin^2 Delta_21 (kShared)
   const int lane = threadIdx.x & 31;
   const int S = 32 >> lv;
   const int64_t tile = blockIdx.x / S;  // (point group, bin tile)
@@ -645,6 +665,24 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   }
   const double c0 = w.c0[pp];
   __syncwarp();
+  // shared (2,1) phase: the same kq21 on every lane for every baseline -> evaluate its sin^2
+  // once per (bin, node) of the tile (lane = bin) instead of once per point
+  bool shared = false;
+  if constexpr (!kMixed && GNA_BATCH_PT_SHARED21) {
+    shared = true;
+#pragma unroll
+    for (int j = 0; j < NT; j += 3) {
+      const double k21 = __shfl_sync(0xffffffffu, kq[j], 0);
+      shared = shared && __all_sync(0xffffffffu, kq[j] == k21);
+    }
+    if (shared) {
+#pragma unroll
+      for (int j = 0; j < NT; j += 3)
+        for (int i = 0; i < order; ++i)
+          sS[((j / 3) * order + i) * 32 + lane] = gna::sin2c(kq[j], sE[i * 32 + lane]);
+      __syncwarp();
+    }
+  }
   double* __restrict__ out = spectra ? spectra + pp * nbins : nullptr;
   // fp64: a ragged last tile (nbins not a multiple of 32) skips its empty bins in a separate
   // copy of the loop, so full tiles run the branch-free one (cfg4 363.0 -> 364.2 G/s).  Mixed
@@ -654,6 +692,12 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   if constexpr (kMixed)
     x2 = pt_tile<2, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0, nbins,
                                          out, pact, sub, lv);
+  else if (shared)
+    x2 = k0 + 32 <= nbins
+             ? pt_tile<0, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
+                                                     k0, nbins, out, pact, sub, lv, sS)
+             : pt_tile<1, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
+                                                     k0, nbins, out, pact, sub, lv, sS);
   else
     x2 = k0 + 32 <= nbins
              ? pt_tile<0, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,

@@ -507,6 +507,39 @@ def test_batch_points_across_lanes_path_vs_oracle_and_bitwise(gna, nbase, nbins,
     assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
+@pytest.mark.parametrize("nbase,nbins,order,odd_every", [(1, 1000, 10, 0), (2, 300, 5, 0),
+                                                         (1, 257, 7, 41), (2, 33, 32, 97),
+                                                         (1, 1, 1, 0)])
+def test_batch_points_across_lanes_shared_dm2_21_bitwise_and_vs_oracle(gna, nbase, nbins, order,
+                                                                        odd_every):
+    """A scan over (theta13, dm2_31) with the solar parameters fixed (cfg4's structure): the
+    points-across-lanes kernel evaluates sin^2 Delta_21 once per warp instead of once per
+    point.  Every point must keep its bits (equal to the per-point / points-inner kernels of
+    100-point calls) and match the oracle; with odd_every > 0 some points carry another dm2_21,
+    so their warps take the general path and the rest the shared one within one call."""
+    g = synth.rng(2600 + nbins + order + odd_every)
+    P = 611
+    pts = synth.points_uniform(g, P, dict(theta13=(0.1, 0.2), dm2_31=(2.3e-3, 2.7e-3)))
+    pts = synth.invert_ordering(g, pts)
+    if odd_every:
+        pts["dm2_21"] = pts["dm2_21"].copy()
+        pts["dm2_21"][::odd_every] = 7.9e-5
+    L = g.uniform(1.0, 300.0, nbase)
+    om = g.uniform(0.1, 2.0, nbase)
+    edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
+    data = synth.pseudo_data(g, edges, om.sum())
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data)
+    idx = np.array([0, 31, 32, 41, 300, 610])
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data,
+                            nthreads=_nt())
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, data))
+    for lo, hi in ((0, 100), (100, 200), (500, 611)):
+        s2 = synth.subset_points(pts, np.arange(lo, hi))
+        sps, x2s = _run_batch(gna, s2, L, om, edges, order, data)
+        assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi]), (lo, hi)
+
+
 @pytest.mark.parametrize("nbase,nbins,order", [(1, 257, 7), (2, 300, 5), (1, 100, 10),
                                                (2, 33, 32), (1, 1, 1)])
 def test_batch_mixed_points_across_lanes_vs_oracle_and_bitwise(gna, nbase, nbins, order):

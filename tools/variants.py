@@ -54,6 +54,11 @@ VARIANTS = {
     "pt_b23_s1": dict(GNA_BATCH_PT_BPSM=23, GNA_BATCH_PT_SUB=1),
     "pt_b23_s2": dict(GNA_BATCH_PT_BPSM=23, GNA_BATCH_PT_SUB=2),
     "pt_b24_s4": dict(GNA_BATCH_PT_BPSM=24, GNA_BATCH_PT_SUB=4),
+    "pt_noshared": dict(GNA_BATCH_PT_SHARED21=0),
+    "pt_n10": dict(GNA_BATCH_PT_N10=1),
+    "pt_n10_mb20": dict(GNA_BATCH_PT_N10=1, GNA_BATCH_PT_MINB=20),
+    "pt_s1_sh": dict(GNA_BATCH_PT_SUB=1),
+    "pt_s4_sh": dict(GNA_BATCH_PT_SUB=4),
     "pt_mb20": dict(GNA_BATCH_PT_MINB=20),
     "pt_mb16": dict(GNA_BATCH_PT_MINB=16),
     "pt_mb12": dict(GNA_BATCH_PT_MINB=12),
