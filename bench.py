@@ -871,7 +871,7 @@ def main():
             # pipes, so the roofline is instruction issue (1 warp instruction per SMSP per cycle
             # = 148 x 4 x 32 lanes x clock).  Per sin^2 term: 3 FP64 (rint of y/2, m, h) + 1 F2F
             # + half of a packed pair's FMUL2 + 6 FFMA2 + accumulating FFMA2 = 8.
-            ipp = 3 * MIXED_INSTR_PER_TERM
+            ipp = MIXED_INSTR_PER_TERM * ((2 + 1 / 32) if shared21 else 3)
             peak_issue = SM_COUNT * 4 * 32 * (clk.summary()["sm_max_mhz"] or 1965.0) * 1e6
             ach = launch_units * ipp / (kern_avg_ms * 1e-3)
             roof = {"bound": "alu", "achieved": ach / 1e12, "peak": peak_issue / 1e12,
@@ -879,8 +879,11 @@ def main():
                     "peak_source": "148 SM x 4 SMSP x 32 lanes x sm_max clock (one warp "
                                    "instruction per SMSP per cycle)",
                     "ops_per_energy_point": ipp,
-                    "fp64_frac": launch_units * 9 / (kern_avg_ms * 1e-3) / peak_ops,
+                    "fp64_frac": launch_units * ipp * 3 / 8 / (kern_avg_ms * 1e-3) / peak_ops,
                     "kernel_ms_per_launch": kern_avg_ms}
+            if shared21:
+                roof["shared_dm2_21"] = ("W(h^2) of the (2,1) term evaluated once per warp of "
+                                         "32 points (same dm2_21 and L for every point)")
 
     tr = _ncu_traffic(args.workload if args.precision == "fp64" else args.workload + "_mixed")
     if tr:
@@ -993,10 +996,10 @@ def _verify_gather(args, c, gna, torch, dist, dev, rank, sb, fg):
 
 
 def shared_dm2_21(c, args, units_per_rank) -> bool:
-    """True when the batch runs the points-across-lanes kernel (fp64, >= 256 points on the
-    rank, <= 2 baselines) and every point has the same dm2_21, so that kernel's shared
-    sin^2 Delta_21 path is taken (k_batch.cuh, GNA_BATCH_PT_SHARED21)."""
-    if args.workload not in ("cfg4", "cfg5") or args.precision != "fp64":
+    """True when the batch runs the points-across-lanes kernel (>= 256 points on the rank,
+    <= 2 baselines; fp64 or mixed tier) and every point has the same dm2_21, so that kernel's
+    shared sin^2 Delta_21 path is taken (k_batch.cuh, GNA_BATCH_PT_SHARED21)."""
+    if args.workload not in ("cfg4", "cfg5"):
         return False
     pts = c["points"]
     nbase = c["L_km"].size

@@ -335,8 +335,8 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
 #endif
     const int64_t ng = (pts->npoints + 31) / 32;
     size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);
-    if (!kMixed && GNA_BATCH_PT_SHARED21)  // shared sin^2 Delta_21 per baseline (k_batch.cuh)
-      smem_pt += (size_t)(nterm / 3) * order * 32 * sizeof(double);
+    if (GNA_BATCH_PT_SHARED21)  // shared sin^2 Delta_21 per baseline (k_batch.cuh)
+      smem_pt += (size_t)(nterm / 3) * order * 32 * (kMixed ? sizeof(float) : sizeof(double));
 #if GNA_BATCH_PT_BPSM
     // wave shaping (experiment): pad shared memory so that at most GNA_BATCH_PT_BPSM one-warp
     // blocks fit on an SM (228 KiB per SM, 1 KiB reserved per block)

@@ -519,6 +519,16 @@ __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const gna::f32x2 w2 = gna::f2_pack(wf[j], wf[j]);
+      if (kShared && j % 3 == 0) {
+        // shared W(h^2) of term 21 (fp32, [baseline][node][32 bins]): the packed evaluation is
+        // element-wise, so a node's value does not depend on which node it is paired with
+        const float* sW = reinterpret_cast<const float*>(sS) + ((j / 3) * order + i) * 32 + b;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+          acc2[k] = gna::f2_fma(w2, gna::f2_pack(sW[(2 * k) * 32], sW[(2 * k + 1) * 32]), acc2[k]);
+        if constexpr (N & 1) acc1 = fmaf(wf[j], sW[(N - 1) * 32], acc1);
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < NP; ++k)
         acc2[k] = gna::f2_fma(w2, gna::cos2_w2(gna::mixed_h2(kq[j], iE[2 * k], kq[j], iE[2 * k + 1])),
@@ -626,7 +636,7 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   double* sW = sH + order * 32;     // [32] sum_i h w_i (same order as k_oscprob_batch)
   double* sD = sW + 32;             // [32] data
   double* sID = sD + 32;            // [32] 1 / data
-  double* sS = sID + 32;            // fp64: [NT/3][order][32] shared sin^2 Delta_21 (kShared)
+  double* sS = sID + 32;            // [NT/3][order][32] shared sin^2 Delta_21 (fp64) or W (fp32)
   const int lane = threadIdx.x & 31;
   const int S = 32 >> lv;
   const int64_t tile = blockIdx.x / S;  // (point group, bin tile)
@@ -668,7 +678,7 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   // shared (2,1) phase: the same kq21 on every lane for every baseline -> evaluate its sin^2
   // once per (bin, node) of the tile (lane = bin) instead of once per point
   bool shared = false;
-  if constexpr (!kMixed && GNA_BATCH_PT_SHARED21) {
+  if constexpr (GNA_BATCH_PT_SHARED21) {
     shared = true;
 #pragma unroll
     for (int j = 0; j < NT; j += 3) {
@@ -676,10 +686,16 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
       shared = shared && __all_sync(0xffffffffu, kq[j] == k21);
     }
     if (shared) {
+      float* sSf = reinterpret_cast<float*>(sS);  // mixed tier: W(h^2) in fp32
 #pragma unroll
       for (int j = 0; j < NT; j += 3)
-        for (int i = 0; i < order; ++i)
-          sS[((j / 3) * order + i) * 32 + lane] = gna::sin2c(kq[j], sE[i * 32 + lane]);
+        for (int i = 0; i < order; ++i) {
+          if constexpr (kMixed)
+            sSf[((j / 3) * order + i) * 32 + lane] =
+                gna::cos2_w(gna::mixed_h1(kq[j], sE[i * 32 + lane]));
+          else
+            sS[((j / 3) * order + i) * 32 + lane] = gna::sin2c(kq[j], sE[i * 32 + lane]);
+        }
       __syncwarp();
     }
   }
@@ -689,9 +705,14 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   // tier: one loop that computes every bin and drops the empty ones — the second loop copy
   // cost it 7 % (556 -> 518 G/s).
   double x2;
-  if constexpr (kMixed)
-    x2 = pt_tile<2, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0, nbins,
-                                         out, pact, sub, lv);
+  if constexpr (kMixed) {
+    if (shared)
+      x2 = pt_tile<2, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+                                                 nbins, out, pact, sub, lv, sS);
+    else
+      x2 = pt_tile<2, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+                                           nbins, out, pact, sub, lv);
+  }
   else if (shared)
     x2 = k0 + 32 <= nbins
              ? pt_tile<0, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,

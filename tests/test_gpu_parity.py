@@ -507,11 +507,12 @@ def test_batch_points_across_lanes_path_vs_oracle_and_bitwise(gna, nbase, nbins,
     assert np.array_equal(sp, sp2) and np.array_equal(x2, x22)
 
 
+@pytest.mark.parametrize("precision", ["fp64", "mixed"])
 @pytest.mark.parametrize("nbase,nbins,order,odd_every", [(1, 1000, 10, 0), (2, 300, 5, 0),
                                                          (1, 257, 7, 41), (2, 33, 32, 97),
                                                          (1, 1, 1, 0)])
 def test_batch_points_across_lanes_shared_dm2_21_bitwise_and_vs_oracle(gna, nbase, nbins, order,
-                                                                        odd_every):
+                                                                        odd_every, precision):
     """A scan over (theta13, dm2_31) with the solar parameters fixed (cfg4's structure): the
     points-across-lanes kernel evaluates sin^2 Delta_21 once per warp instead of once per
     point.  Every point must keep its bits (equal to the per-point / points-inner kernels of
@@ -528,15 +529,18 @@ def test_batch_points_across_lanes_shared_dm2_21_bitwise_and_vs_oracle(gna, nbas
     om = g.uniform(0.1, 2.0, nbase)
     edges = np.sort(g.uniform(1.0, 10.0, nbins + 1))
     data = synth.pseudo_data(g, edges, om.sum())
-    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data)
+    sp, x2 = _run_batch(gna, pts, L, om, edges, order, data, precision=precision)
     idx = np.array([0, 31, 32, 41, 300, 610])
     spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data,
                             nthreads=_nt())
-    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
-    assert np.all(np.abs(x2[idx] - x2r) <= _chi2_bound(spr, data))
+    tol = TOL_BIN if precision == "fp64" else TOL_MIXED
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= tol
+    bound = (_chi2_bound(spr, data) if precision == "fp64" else
+             _chi2_bound_tol(spr, data, TOL_MIXED))
+    assert np.all(np.abs(x2[idx] - x2r) <= bound)
     for lo, hi in ((0, 100), (100, 200), (500, 611)):
         s2 = synth.subset_points(pts, np.arange(lo, hi))
-        sps, x2s = _run_batch(gna, s2, L, om, edges, order, data)
+        sps, x2s = _run_batch(gna, s2, L, om, edges, order, data, precision=precision)
         assert np.array_equal(sps, sp[lo:hi]) and np.array_equal(x2s, x2[lo:hi]), (lo, hi)
 
 
