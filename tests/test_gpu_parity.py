@@ -901,6 +901,12 @@ def test_fused_gather_epilogue_single_rank(gna, P, nbase):
             assert np.array_equal(_np(sp), ref_sp) and np.array_equal(_np(x2), ref_x2)
             seen.append(flags)
         assert gna.GNA_OUT_PEER in seen
+        # and the window's contents against the oracle (not only against the CUDA batch)
+        idx = np.unique(np.r_[0, P // 2, P - 1])
+        spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, 10, data=data,
+                                nthreads=_nt())
+        assert np.max(np.abs(ref_sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+        assert np.all(np.abs(ref_x2[idx] - x2r) <= _chi2_bound(spr, data))
     finally:
         dist.destroy_process_group()
 
