@@ -39,8 +39,21 @@ def padded_rows(npoints: int, world: int) -> int:
 
 
 def chunk_bounds(rows: int, chunks: int) -> list[tuple[int, int]]:
+    """Row ranges of the gather pipeline's chunks, tapered: chunk c gets a share proportional
+    to chunks - c (4 chunks: 4:3:2:1), so that the last chunk — whose all-gather is the only
+    one not hidden under a later chunk's kernel — is the smallest.  Every chunk is non-empty
+    while rows >= chunks."""
     chunks = max(1, min(chunks, max(rows, 1)))
-    return [(c * rows // chunks, (c + 1) * rows // chunks) for c in range(chunks)]
+    wsum = chunks * (chunks + 1) // 2
+    bounds, acc = [], 0
+    for c in range(chunks):
+        acc += chunks - c
+        hi = rows * acc // wsum
+        lo = bounds[-1][1] if bounds else 0
+        hi = max(hi, min(rows, lo + 1))  # non-empty when rows allow
+        bounds.append((lo, hi))
+    bounds[-1] = (bounds[-1][0], rows)
+    return bounds
 
 
 def gather_index(npoints: int, world: int, chunks: int = 1) -> np.ndarray:
