@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <algorithm>
 #include <complex>
@@ -557,6 +558,15 @@ constexpr int kRing = 3;
 #ifndef GNA_HOST_SPECTRA_MAX
 #define GNA_HOST_SPECTRA_MAX (1ull << 31)  // device bytes for un-ringed batch spectra staging
 #endif
+// the environment variable of the same name overrides it (read once; tests use it to run
+// the ring path at small sizes)
+size_t host_spectra_max() {
+  static const size_t v = [] {
+    const char* e = std::getenv("GNA_HOST_SPECTRA_MAX");
+    return e ? (size_t)std::strtoull(e, nullptr, 10) : (size_t)GNA_HOST_SPECTRA_MAX;
+  }();
+  return v;
+}
 struct Staging {
   bool init = false;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};
@@ -1067,7 +1077,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   // spectra: one region per point (no reuse, the kernels never wait for a copy) when all of
   // them fit in GNA_HOST_SPECTRA_MAX bytes, else a ring of kRing chunk slots
   const size_t b_all = align16((size_t)P * nbins * 8);
-  const bool out_ring = h_spectra && b_all > (size_t)GNA_HOST_SPECTRA_MAX;
+  const bool out_ring = h_spectra && b_all > host_spectra_max();
   const size_t b_slot = h_spectra ? align16((size_t)chunk_points * nbins * 8) : 0;
   const size_t b_spec = !h_spectra ? 0 : out_ring ? kRing * b_slot : b_all;
   if ((rc = ensure(&S->buf, &S->cap, tb + b_edges + b_data + b_pts + b_chi + b_ws + b_spec)))

@@ -743,6 +743,49 @@ def test_batch_host_bitwise_equals_device(gna):
     assert np.array_equal(x2h2, x2d)
 
 
+_HOST_RING_SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %(root)r)
+import torch
+import paper_1804_07682_b200 as gna
+import synth
+g = synth.rng(54)
+P, nb, order = 300, 257, 6
+pts = synth.invert_ordering(g, synth.points_uniform(g, P, dict(
+    theta12=(0.5, 0.65), theta13=(0.1, 0.2), dm2_21=(6e-5, 9e-5), dm2_31=(2.2e-3, 2.8e-3))))
+L, om = np.array([52.5, 215.0, 1.0]), np.array([1.0, 0.1, 0.3])
+edges = np.sort(g.uniform(1.0, 10.0, nb + 1))
+data = synth.pseudo_data(g, edges, om.sum())
+for cp in (40, 7, 300):  # tapered tails through a 3-slot ring; a single chunk
+    sph, x2h = gna.oscprob_batch_host(pts, L, om, edges, order, data=data, chunk_points=cp)
+    spd, x2d = gna.oscprob_batch({k: torch.tensor(v, device="cuda") for k, v in pts.items()}, L,
+                                 om, torch.tensor(edges, device="cuda"), order,
+                                 data=torch.tensor(data, device="cuda"))
+    assert np.array_equal(sph, spd.cpu().numpy()) and np.array_equal(x2h, x2d.cpu().numpy()), cp
+print("RING_OK")
+"""
+
+
+@pytest.mark.parametrize("spectra_max", ["1", "0"])
+def test_batch_host_ring_and_tapered_chunks_bitwise(gna, spectra_max):
+    """Host-buffer batch with tapered chunk plans, through the 3-slot spectra ring (forced by
+    GNA_HOST_SPECTRA_MAX=1 byte, as for spectra larger than 2 GiB) and through the per-point
+    staging regions (GNA_HOST_SPECTRA_MAX unset): bitwise equal to the device call.  Runs in a
+    subprocess because the library reads the variable once."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    if spectra_max != "0":
+        env["GNA_HOST_SPECTRA_MAX"] = spectra_max
+    else:
+        env.pop("GNA_HOST_SPECTRA_MAX", None)
+    r = subprocess.run([sys.executable, "-c", _HOST_RING_SCRIPT % dict(root=root)],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0 and "RING_OK" in r.stdout, r.stderr[-3000:]
+
+
 # ------------------------------------------------------------------------ streams and graphs
 def test_batch_capturable_in_cuda_graph(gna):
     """The device entry points are stream-ordered and allocation-free: they can be captured
