@@ -179,3 +179,77 @@ def test_fused_probe_runs_on_one_rank():
                            capture_output=True, text=True, timeout=300, env=env, cwd=root)
         assert r.returncode == 0, r.stderr[-3000:]
         assert "FUSED_PROBE_OK peer-to-root" in r.stdout, (r.stdout[-2000:], r.stderr[-2000:])
+
+
+def _ipc_writer(rank, world, q_buf, q_done, P, nb):
+    """Rank r > 0: receive the root's output tensors (CUDA IPC mapping of another process's
+    allocation) and write its rows through the fused epilogue (GNA_OUT_PEER)."""
+    import torch
+
+    import paper_1804_07682_b200 as gna
+    from paper_1804_07682_b200 import dist as gdist
+    torch.cuda.set_device(0)
+    sp_root, x2_root = q_buf.get()
+    pts, L, om, edges, order, data = _case(P=P, nbins=nb)
+    lo, hi = gdist.shard_range(P, world, rank)
+    f64 = dict(dtype=torch.float64, device="cuda")
+    mine = {k: torch.tensor(v[lo:hi], **f64) for k, v in pts.items()}
+    gna.oscprob_batch_ex(mine, L, om, torch.tensor(edges, **f64), order,
+                         sp_root.data_ptr() + lo * nb * 8, x2_root.data_ptr() + lo * 8,
+                         gna.GNA_OUT_PEER, data=torch.tensor(data, **f64))
+    torch.cuda.synchronize()
+    q_done.put(rank)
+    q_buf.get()  # keep the mapping alive until the root has read the result
+
+
+def test_peer_epilogue_writes_another_process_buffer_one_gpu(tmp_path):
+    """The fused epilogue's peer stores across a process boundary, on one GPU: rank 0 owns the
+    gathered spectra / chi^2 buffers, ranks 1-2 (separate processes, CUDA IPC mappings of
+    rank 0's allocations) write their rows with gna_oscprob_batch_ex(GNA_OUT_PEER) while rank 0
+    writes its own; no kernel waits on another process (host-side hand-off only).  The buffer
+    must equal one local batch bit for bit and the oracle on sampled points.  NVLink is not
+    involved (one GPU); the window arithmetic and the remote-store epilogue are."""
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_1804_07682_b200 as gna
+    from paper_1804_07682_b200 import dist as gdist
+    if _ngpus() < 1:
+        pytest.skip("no GPU")
+    P, nb, world = 37, 257, 3
+    pts, L, om, edges, order, data = _case(P=P, nbins=nb)
+    f64 = dict(dtype=torch.float64, device="cuda")
+    sp = torch.full((P, nb), float("nan"), **f64)
+    x2 = torch.full((P,), float("nan"), **f64)
+    ctx = mp.get_context("spawn")
+    q_buf, q_done = ctx.Queue(), ctx.Queue()
+    procs = [ctx.Process(target=_ipc_writer, args=(r, world, q_buf, q_done, P, nb))
+             for r in range(1, world)]
+    for p in procs:
+        p.start()
+    for _ in procs:
+        q_buf.put((sp, x2))
+    de, dd = torch.tensor(edges, **f64), torch.tensor(data, **f64)
+    lo, hi = gdist.shard_range(P, world, 0)
+    gna.oscprob_batch_ex({k: torch.tensor(v[lo:hi], **f64) for k, v in pts.items()}, L, om, de,
+                         order, sp.data_ptr() + lo * nb * 8, x2.data_ptr() + lo * 8,
+                         gna.GNA_OUT_PEER, data=dd)
+    torch.cuda.synchronize()
+    done = sorted(q_done.get(timeout=300) for _ in procs)
+    assert done == list(range(1, world))
+    got_sp, got_x2 = sp.cpu().numpy(), x2.cpu().numpy()
+    for _ in procs:
+        q_buf.put(None)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref_sp, ref_x2 = gna.oscprob_batch({k: torch.tensor(v, **f64) for k, v in pts.items()}, L, om,
+                                       de, order, data=dd)
+    assert np.array_equal(got_sp, ref_sp.cpu().numpy()) and np.array_equal(got_x2,
+                                                                           ref_x2.cpu().numpy())
+    idx = np.array([0, 12, 13, 24, 25, 36])  # both sides of every shard boundary
+    spr, x2r = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data)
+    assert np.max(np.abs(got_sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
+    d = np.abs(spr - data)
+    bound = np.sum((2 * d * TOL_BIN * np.abs(spr) + d * d * 8 * EPS) / data, axis=-1)
+    assert np.all(np.abs(got_x2[idx] - x2r) <= bound + 1e-300)
