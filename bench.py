@@ -783,7 +783,8 @@ def main():
         torch.cuda.synchronize()
     barrier()
     launches = gna.launch_count() - n_launch0
-    total_ms = sum(a.elapsed_time(b) for a, b in evs)
+    step_times = sorted(a.elapsed_time(b) for a, b in evs)
+    total_ms = sum(step_times)
     if use_graph:
         # kernels replayed from the graph: count = per-step launches captured x steps;
         # the step is the dominant kernel plus two us-scale helpers -> step time bounds it
@@ -911,6 +912,9 @@ def main():
                            l2="flushed between steps (256 MiB write, untimed)",
                            energy_points_per_step=units_total),
             "bins_per_s": (c["bins_total"] * args.steps / (total_ms * 1e-3)) if c["bins_total"] else None,
+            # this rank's per-step device times (median and min next to the mean)
+            "step_ms": {"median": step_times[len(step_times) // 2], "min": step_times[0],
+                        "max": step_times[-1]},
             "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof,
             "cuda_graph": bool(use_graph)}
     if args.workload in ("cfg4", "cfg5"):
