@@ -744,19 +744,44 @@ def main():
 
     # ---------------- CUDA graph of the step (the repeated-evaluation loop of a fit):
     # one graph launch per step instead of per-call host work.  NCCL steps stay eager.
+    # CUDA graph of the whole step.  At N > 1 the NCCL path is captured too (its chunk kernels
+    # and all-gathers on the communication stream): eagerly, enqueueing one chunk costs ~100 us
+    # of host time (34 us per batch call, 31 us per all-gather; tools/host_overhead_probe.py),
+    # which at G = 8 would exceed the chunk's GPU time.  Every rank must capture successfully,
+    # else all run eagerly.  The fused epilogue (symmetric-memory barrier) and gloo stay eager.
     fused_used = args.workload in ("cfg4", "cfg5") and fused_fg is not None
-    use_graph = args.graph == "on" or (args.graph == "auto" and world == 1 and not fused_used)
+    use_graph = args.graph == "on" or (args.graph == "auto" and not fused_used and
+                                       (world == 1 or args.backend == "nccl"))
     launches_per_step = None
+    graph_note = None
     if use_graph:
         KernelTimer.enabled = False
         g = torch.cuda.CUDAGraph()
         n0 = gna.launch_count()
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(cap):
-            with torch.cuda.graph(g, stream=cap):
-                step()
+        captured = True
+        try:
+            with torch.cuda.stream(cap):
+                with torch.cuda.graph(g, stream=cap):
+                    step()
+        except Exception as exc:  # noqa: BLE001 — reported; the run continues eagerly
+            captured = False
+            graph_note = "capture failed, eager steps: %s" % (str(exc).splitlines()[0][:120]
+                                                            if str(exc) else type(exc).__name__)
         torch.cuda.current_stream().wait_stream(cap)
+        torch.cuda.synchronize()
+        if world > 1:
+            agree = torch.tensor([1.0 if captured else 0.0], device=dev)
+            dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+            if float(agree) != 1.0 and captured:
+                graph_note = "capture failed on another rank, eager steps"
+            captured = float(agree) == 1.0
+        use_graph = captured
+        if not captured:
+            KernelTimer.enabled = True
+            kern_ev.clear()
+    if use_graph:
         launches_per_step = gna.launch_count() - n0
         eager_step = step
 
@@ -838,8 +863,9 @@ def main():
                 "fp64_frac": launch_units * fp64_eval / (kern_avg_ms * 1e-3) / peak_ops,
                 "fp64_ops_per_energy": fp64_eval}
     else:
+        # per library call, or per graph-replayed step (then the step time is the kernel time)
         launch_units = (units_per_rank / max(calls_per_step, 1)
-                        if args.workload in ("cfg4", "cfg5") else units_per_rank)
+                        if args.workload in ("cfg4", "cfg5") and not use_graph else units_per_rank)
         per_point_ops = ops_eval
         shared21 = shared_dm2_21(c, args, units_per_rank)
         if shared21:
@@ -917,6 +943,8 @@ def main():
                         "max": step_times[-1]},
             "clocks": clk.summary(), "gpu_launches": launches, "roofline": roof,
             "cuda_graph": bool(use_graph)}
+    if graph_note:
+        line["cuda_graph_note"] = graph_note
     if args.workload in ("cfg4", "cfg5"):
         line["config"]["gather"] = gather_mode
         line["config"]["gather_chunks"] = len(sb.cb)

@@ -253,3 +253,74 @@ def test_peer_epilogue_writes_another_process_buffer_one_gpu(tmp_path):
     d = np.abs(spr - data)
     bound = np.sum((2 * d * TOL_BIN * np.abs(spr) + d * d * 8 * EPS) / data, axis=-1)
     assert np.all(np.abs(got_x2[idx] - x2r) <= bound + 1e-300)
+
+
+def test_sharded_step_with_nccl_capturable_in_cuda_graph_one_rank():
+    """bench.py captures the N > 1 NCCL step in a CUDA graph (chunk kernels on the current
+    stream, all-gathers on the communication stream); here the same dist.ShardedBatch.step is
+    captured with a one-rank NCCL group — the collectives are still NCCL calls inside the
+    capture — and the replayed result equals the eager one and the oracle."""
+    import subprocess
+    import sys
+    if _ngpus() < 1:
+        pytest.skip("no GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r'''
+import sys, socket
+import numpy as np
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+import torch, torch.distributed as dist
+import paper_1804_07682_b200 as gna
+from paper_1804_07682_b200 import dist as gdist
+import test_multigpu as tm
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%%d" %% port, rank=0, world_size=1,
+                        device_id=torch.device("cuda", 0))
+pts, L, om, edges, order, data = tm._case()
+P, nb = pts["theta12"].size, edges.size - 1
+f64 = dict(dtype=torch.float64, device="cuda")
+de, dd = torch.tensor(edges, **f64), torch.tensor(data, **f64)
+sb = gdist.ShardedBatch(P, nb, 1, 0, chunks=3).allocate("cuda")
+mine = {k: torch.tensor(v, **f64) for k, v in pts.items()}
+ws = torch.empty(gna.oscprob_batch_workspace_size(P, L.size, nb, order) // 8 + 2, **f64)
+def compute(vlo, vhi, sp_rows, x2_rows):
+    gna.oscprob_batch({k: v[vlo:vhi] for k, v in mine.items()}, L, om, de, order, data=dd,
+                      spectra=sp_rows, chi2=x2_rows, workspace=ws, tables_valid=vlo > 0)
+comm = torch.cuda.Stream()
+# one rank: step() gathers nothing, so drive the chunk gathers explicitly as bench does at N > 1
+def step():
+    works = []
+    for c, (lo, hi) in enumerate(sb.cb):
+        compute(lo, min(hi, sb.count), sb.spectra[lo:hi], sb.chi2[lo:hi])
+        ev = torch.cuda.Event(); ev.record()
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev)
+            works += sb._gather_chunk(c, lo, hi, dist)
+    for w in works:
+        w.wait()
+    torch.cuda.current_stream().wait_stream(comm)
+step(); torch.cuda.synchronize()
+ref = torch.cat([gs for gs in sb.g_spectra]).clone()
+for gs in sb.g_spectra: gs.zero_()
+g = torch.cuda.CUDAGraph()
+cap = torch.cuda.Stream(); cap.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(cap), torch.cuda.graph(g, stream=cap):
+    step()
+torch.cuda.current_stream().wait_stream(cap)
+g.replay(); torch.cuda.synchronize()
+got = torch.cat([gs for gs in sb.g_spectra])
+assert torch.equal(got, ref)
+np.save(%r, got.cpu().numpy())
+dist.destroy_process_group()
+print("CAPTURE_OK")
+''' % (root, os.path.join(root, "tests"), os.path.join(root, "build", "nccl_capture_sp.npy"))
+    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True,
+                       timeout=300, cwd=root)
+    assert r.returncode == 0 and "CAPTURE_OK" in r.stdout, r.stderr[-3000:]
+    pts, L, om, edges, order, data = _case()
+    sp = np.load(os.path.join(root, "build", "nccl_capture_sp.npy"))
+    idx = np.array([0, 18, 36])
+    spr, _ = oracle.batch(synth.subset_points(pts, idx), L, om, edges, order, data=data)
+    assert np.max(np.abs(sp[idx] - spr) / np.abs(spr)) <= TOL_BIN
