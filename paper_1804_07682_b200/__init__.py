@@ -340,6 +340,8 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
     if data is not None and chi2 is None:
         chi2 = torch.empty(P, dtype=torch.float64, device=dev)
     Lh, om = _baselines(L_km, omega)
+    if tables_valid and workspace is None:
+        raise ValueError("tables_valid needs the workspace that holds the tables")
     b = _CBatch(*(_dev(points[k], k, P) for k in ("theta12", "theta13", "dm2_21", "dm2_31")), P)
     if workspace is None:
         workspace = _scratch(oscprob_batch_workspace_size(P, Lh.size, nbins, order), dev, stream)
@@ -349,8 +351,6 @@ def oscprob_batch(points: dict, L_km, omega, edges, order: int, data=None, spect
             _dev(chi2, "chi2", P) if chi2 is not None else None,
             _dev(workspace, "workspace"), workspace.numel() * 8)
     flags = _prec_flags(precision) | (GNA_WS_TABLES_VALID if tables_valid else 0)
-    if tables_valid and workspace is None:
-        raise ValueError("tables_valid needs the workspace that holds the tables")
     if flags:
         _check(L.gna_oscprob_batch_ex(*args, flags, _stream(stream)), "gna_oscprob_batch_ex")
     else:

@@ -431,3 +431,14 @@ def test_binding_checks_lengths_before_any_call(lib):
     with pytest.raises(ValueError):
         gna.fit_pattern_search(torch.zeros(8, dtype=torch.float64), [52.5, 215.0], [1.0],
                                torch.tensor(edges), 5, torch.tensor(data), 1)
+
+
+def test_tables_valid_needs_a_workspace(lib):
+    """tables_valid=True without the workspace that holds the tables is refused before any
+    call (a fresh scratch workspace would hold no tables)."""
+    import torch
+    pts = {k: torch.zeros(3, dtype=torch.float64) for k in ("theta12", "theta13", "dm2_21",
+                                                           "dm2_31")}
+    with pytest.raises(ValueError):
+        gna.oscprob_batch(pts, [52.5], [1.0], torch.linspace(1, 10, 11, dtype=torch.float64), 5,
+                          tables_valid=True)
