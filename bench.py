@@ -410,16 +410,27 @@ def isolated_fused_probe(args, world, rank, dist):
         res = {"ok": False, "why": "probe did not run"}
         t0 = time.time()
         try:
-            out = subprocess.run(cmd, capture_output=True, text=True, env=env,
-                                 timeout=args.probe_timeout)
-            ok_lines = [l for l in out.stdout.splitlines() if l.startswith("FUSED_PROBE_OK")]
-            if out.returncode == 0 and ok_lines:
-                res = {"ok": True, "mode": ok_lines[-1].split()[1]}
-            else:
-                tail = (out.stdout + out.stderr).strip().splitlines()[-1:] or ["no output"]
-                res = {"ok": False, "why": "probe rc=%d: %s" % (out.returncode, tail[0][:160])}
-        except subprocess.TimeoutExpired:
-            res = {"ok": False, "why": "probe timed out after %.0f s" % args.probe_timeout}
+            # own session: on a timeout the launcher AND its worker ranks (which may be stuck
+            # in a device-side wait) are killed as one process group, so none keeps a GPU busy
+            proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                    text=True, env=env, start_new_session=True)
+            try:
+                so, se = proc.communicate(timeout=args.probe_timeout)
+                ok_lines = [l for l in so.splitlines() if l.startswith("FUSED_PROBE_OK")]
+                if proc.returncode == 0 and ok_lines:
+                    res = {"ok": True, "mode": ok_lines[-1].split()[1]}
+                else:
+                    tail = (so + se).strip().splitlines()[-1:] or ["no output"]
+                    res = {"ok": False, "why": "probe rc=%d: %s" % (proc.returncode,
+                                                                    tail[0][:160])}
+            except subprocess.TimeoutExpired:
+                import signal
+                try:
+                    os.killpg(proc.pid, signal.SIGKILL)
+                except OSError:
+                    pass
+                proc.communicate()
+                res = {"ok": False, "why": "probe timed out after %.0f s" % args.probe_timeout}
         except OSError as exc:
             res = {"ok": False, "why": "probe failed to start: %s" % exc}
         res["seconds"] = round(time.time() - t0, 1)
