@@ -68,6 +68,36 @@ def main():
             for d in ("d2h", "h2d"):
                 res.append({"bytes": size, "streams": ns, "dir": d, "GBps": round(bw(size, ns, d), 2)})
     out["default"] = res
+    # both directions at once (separate copy engines): the ceiling of the elementwise e2e path,
+    # which streams its input up while the results of earlier chunks come back
+    n = 256 << 20
+    a_d = torch.empty(n // 8, dtype=torch.float64, device="cuda")
+    b_d = torch.empty(n // 8, dtype=torch.float64, device="cuda")
+    a_h = torch.empty(n // 8, dtype=torch.float64).pin_memory()
+    b_h = torch.empty(n // 8, dtype=torch.float64).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def both():
+        s1.wait_stream(torch.cuda.current_stream())
+        s2.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s1):
+            a_d.copy_(a_h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            b_h.copy_(b_d, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(s1)
+        torch.cuda.current_stream().wait_stream(s2)
+    both()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        both()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    out["bidirectional_256MB_each"] = {"ms": round(ms, 3),
+                                       "GBps_per_direction": round(n / (ms * 1e-3) / 1e9, 2),
+                                       "GBps_total": round(2 * n / (ms * 1e-3) / 1e9, 2)}
     # pin from a CPU on the GPU's NUMA node (first touch decides the page's node)
     if node is not None and node >= 0:
         try:
