@@ -468,10 +468,22 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   if (e != cudaSuccess) return cuda_fail(e);
   const bool vec2 = (nbins & 1) == 0 && ((uintptr_t)spectra & 15) == 0 &&
                     (!chi2 || ((uintptr_t)data & 15) == 0);
-  if (GNA_SCAN_EXPAND2 && vec2)
-    k_scan_expand2<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
-                                                           chi2 ? data : nullptr, chi2);
-  else
+  if (GNA_SCAN_EXPAND2 && vec2) {
+    // bin chunks only when the grid gives fewer than 4 blocks per SM on its own
+    const int64_t nbc = nblk < 4 * sm_count() ? scan_nbc(nbins) : 1;
+    if (nblk * nbc > 0x7fffffffLL) return GNA_EINVAL;
+    if (nbc > 1)
+      k_scan_expand2<true><<<(unsigned)(nblk * nbc), kScanThreads, 0, s>>>(
+          g->nmix, nbins, nchunk, w, spectra, chi2 ? data : nullptr, chi2);
+    else
+      k_scan_expand2<false><<<(unsigned)nblk, kScanThreads, 0, s>>>(
+          g->nmix, nbins, nchunk, w, spectra, chi2 ? data : nullptr, chi2);
+    if (chi2 && nbc > 1) {
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      const int64_t np = g->nmass * g->nmix;
+      k_scan_chi2_fold<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(w.partial, np, nbc, chi2);
+    }
+  } else
     k_scan_expand<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
                                                           chi2 ? data : nullptr, chi2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -929,6 +941,9 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
 size_t gna_fit_workspace_size(int32_t nbase, int64_t nbins, int32_t order) {
   if (nbase < 1 || nbase > GNA_MAX_NBASE || nbins < 1 || order < 1 || order > GNA_MAX_ORDER)
     return 0;
+  if (GNA_FIT_SCAN)  // grid [4][9] | chi2 [81] | scan workspace (32-byte aligned pieces)
+    return align32((size_t)kFitDim * kFitGrid * 8) + align32((size_t)kFitCand * 8) +
+           scan_ws_bytes(kFitGrid, kFitGrid, nbins) + 32;
   return align16((size_t)kFitDim * kFitCand * 8) + align16((size_t)kFitCand * 8) +
          batch_ws_bytes(kFitCand, nbase, nbins, order, true);
 }
@@ -950,6 +965,31 @@ int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbas
   for (const void* q : ptrs)
     if (q && check_dev_ptr(q)) return GNA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  if (GNA_FIT_SCAN) {
+    // one 9 x 9 separable scan per iteration (k_fit.cuh)
+    char* w = (char*)(((uintptr_t)d_workspace + 31) & ~(uintptr_t)31);
+    double* grid = (double*)w;
+    w += align32((size_t)kFitDim * kFitGrid * 8);
+    double* chi2 = (double*)w;
+    w += align32((size_t)kFitCand * 8);
+    void* sws = w;
+    const gna_scan_grid g = {grid, grid + kFitGrid, kFitGrid, grid + 2 * kFitGrid,
+                             grid + 3 * kFitGrid, kFitGrid};
+    if (niter > 0) {
+      k_fit_grid<<<1, 128, 0, s>>>(d_state, grid);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    for (int it = 0; it < niter; ++it) {
+      if ((rc = launch_scan(&g, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data, chi2,
+                            sws, s)))
+        return rc;
+      k_fit_update_grid<<<1, 128, 0, s>>>(d_state, grid, chi2, d_hist, it, it + 1 < niter);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return GNA_OK;
+  }
   char* w = (char*)d_workspace;
   double* cand = (double*)w;
   w += align16((size_t)kFitDim * kFitCand * 8);

@@ -74,4 +74,84 @@ __global__ void __launch_bounds__(128) k_fit_update(double* __restrict__ state,
   }
 }
 
+// ----------------------------------------------------------------------------
+// Separable stencil (GNA_FIT_SCAN, default): the 81 candidates are the Cartesian product of 9
+// mixing points (theta12, theta13) and 9 mass points (dm2_21, dm2_31), and candidate
+// c = i0 + 3 i1 + 9 i2 + 27 i3 is mixing point i0 + 3 i1 of mass point i2 + 3 i3 — exactly the
+// NEXT-1 scan's point order (mass-major).  So one iteration is one gna_oscprob_scan over a
+// 9 x 9 grid: the binned sin^2 sums are formed for 9 mass points instead of 81 candidates
+// (P:439-440), and the mixing weights enter linearly.  Candidate coordinates are the same
+// fma(o, step, centre) values as fit_candidate's, so the state sequence is unchanged whenever
+// the argmin is.
+#ifndef GNA_FIT_SCAN
+#define GNA_FIT_SCAN 1
+#endif
+constexpr int kFitGrid = 9;  // 3^2 mixing points, 3^2 mass points
+
+// grid arrays [theta12[9] | theta13[9] | dm2_21[9] | dm2_31[9]] of the current state
+__device__ __forceinline__ void fit_grid(const double* __restrict__ state,
+                                         double* __restrict__ grid, int t) {
+  if (t < kFitGrid) {
+    const int o0 = t % 3 - 1, o1 = t / 3 - 1;
+    grid[t] = fma((double)o0, state[kFitDim + 0], state[0]);
+    grid[kFitGrid + t] = fma((double)o1, state[kFitDim + 1], state[1]);
+    grid[2 * kFitGrid + t] = fma((double)o0, state[kFitDim + 2], state[2]);
+    grid[3 * kFitGrid + t] = fma((double)o1, state[kFitDim + 3], state[3]);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_fit_grid(const double* __restrict__ state,
+                                                  double* __restrict__ grid) {
+  fit_grid(state, grid, threadIdx.x);
+}
+
+// argmin + move/halve as k_fit_update; the best candidate's coordinates are rebuilt from the
+// old state (the same fma as fit_candidate), then the next grid is written
+__global__ void __launch_bounds__(128) k_fit_update_grid(double* __restrict__ state,
+                                                         double* __restrict__ grid,
+                                                         const double* __restrict__ chi2,
+                                                         double* __restrict__ hist, int iter,
+                                                         int next_grid) {
+  __shared__ double s_v[128];
+  __shared__ int s_i[128];
+  const int t = threadIdx.x;
+  s_v[t] = t < kFitCand ? chi2[t] : INFINITY;
+  s_i[t] = t;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {  // argmin, ties -> lowest index (deterministic)
+    if (t < o) {
+      const double a = s_v[t], b = s_v[t + o];
+      if (b < a || (b == a && s_i[t + o] < s_i[t])) {
+        s_v[t] = b;
+        s_i[t] = s_i[t + o];
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const int best = s_i[0];
+    const int centre = kFitCand / 2;
+    if (best == centre || !(s_v[0] < chi2[centre])) {
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[kFitDim + d] *= 0.5;
+    } else {
+      double nc[kFitDim];
+      int code = best;
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) {
+        const int o = code % 3 - 1;
+        code /= 3;
+        nc[d] = fma((double)o, state[kFitDim + d], state[d]);
+      }
+#pragma unroll
+      for (int d = 0; d < kFitDim; ++d) state[d] = nc[d];
+    }
+    if (hist) hist[iter] = fmin(s_v[0], chi2[centre]);
+  }
+  if (next_grid) {
+    __syncthreads();  // thread 0's state update is complete
+    fit_grid(state, grid, t);
+  }
+}
+
 }  // namespace

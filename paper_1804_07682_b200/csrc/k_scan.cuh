@@ -31,12 +31,22 @@ struct ScanWs {
   double* H;     // [nbins]
   double* invD;  // [nbins]  1 / data (chi2 only)
   double* wmix;  // [nmix][4]  (w21, w31, w32, 0)
+  double* partial;  // [nmass * nmix][nbc] chi2 per bin chunk (k_scan_expand2, nbc > 1)
 };
+
+// stage B splits the bins into chunks of kScanBinChunk (even) when the grid alone gives too few
+// blocks (the fit's 9 x 9 stencil: 27 blocks for 10^4 bins); chi^2 is then summed from
+// per-chunk partials in chunk order (k_scan_chi2_fold)
+constexpr int64_t kScanBinChunk = 1024;
+__host__ __device__ inline int64_t scan_nbc(int64_t nbins) {
+  return (nbins + kScanBinChunk - 1) / kScanBinChunk;
+}
 
 size_t scan_ws_bytes(int64_t nmix, int64_t nmass, int64_t nbins) {
   size_t b = align32((size_t)nmass * 3 * nbins * sizeof(double));
   b += 2 * align32((size_t)nbins * sizeof(double));
   b += align32((size_t)nmix * 4 * sizeof(double));
+  b += align32((size_t)nmass * nmix * scan_nbc(nbins) * sizeof(double));
   return b;
 }
 
@@ -50,6 +60,8 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
   w.invD = (double*)c;
   c += align32((size_t)nbins * sizeof(double));
   w.wmix = (double*)c;
+  c += align32((size_t)nmix * 4 * sizeof(double));
+  w.partial = (double*)c;
   return w;
 }
 
@@ -250,14 +262,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
 #ifndef GNA_SCAN_EXPAND2
 #define GNA_SCAN_EXPAND2 1
 #endif
+// kChunked: the bins are split into chunks of kScanBinChunk across blocks (chi^2 partials);
+// otherwise one block walks all bins (the round-1 shape, kept for large grids: the chunk
+// bookkeeping alone cost cfg4grid 1.2 us)
+template <bool kChunked>
 __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int64_t nbins,
                                                                int64_t nchunk, ScanWs w,
                                                                double* __restrict__ spectra,
                                                                const double* __restrict__ data,
                                                                double* __restrict__ chi2) {
   __shared__ double s_x2[kScanA][kScanThreads / 32];
-  const int64_t c = blockIdx.x / nchunk;
-  const int64_t a0 = (blockIdx.x - c * nchunk) * kScanA;
+  const int64_t nbc = kChunked ? scan_nbc(nbins) : 1;
+  const int64_t cb = kChunked ? blockIdx.x / nbc : blockIdx.x;  // (mass point, mixing chunk)
+  const int64_t bc = kChunked ? blockIdx.x - cb * nbc : 0;      // bin chunk
+  const int64_t c = cb / nchunk;
+  const int64_t a0 = (cb - c * nchunk) * kScanA;
   const int na = (int)min((int64_t)kScanA, nmix - a0);
   double w0[kScanA], w1[kScanA], w2[kScanA], x2[kScanA];
 #pragma unroll
@@ -278,16 +297,17 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int
   const double2* __restrict__ iDv = reinterpret_cast<const double2*>(w.invD);
   double2* __restrict__ out =
       spectra ? reinterpret_cast<double2*>(spectra + (c * nmix + a0) * nbins) : nullptr;
-  int64_t q = threadIdx.x;
+  const int64_t qend = kChunked ? min(np, (bc + 1) * (kScanBinChunk / 2)) : np;
+  int64_t q = (kChunked ? bc * (kScanBinChunk / 2) : 0) + threadIdx.x;
   double2 G0 = {0, 0}, G1 = {0, 0}, G2 = {0, 0}, H = {0, 0}, D = {0, 0}, iD = {0, 0};
-  if (q < np) {
+  if (q < qend) {
     G0 = g0[q], G1 = g1[q], G2 = g2[q], H = Hv[q];
     if (chi2) D = Dv[q], iD = iDv[q];
   }
-  for (; q < np; q += kScanThreads) {
+  for (; q < qend; q += kScanThreads) {
     const int64_t qn = q + kScanThreads;
     double2 nG0 = {0, 0}, nG1 = {0, 0}, nG2 = {0, 0}, nH = {0, 0}, nD = {0, 0}, niD = {0, 0};
-    if (qn < np) {
+    if (qn < qend) {
       nG0 = g0[qn], nG1 = g1[qn], nG2 = g2[qn], nH = Hv[qn];
       if (chi2) nD = Dv[qn], niD = iDv[qn];
     }
@@ -319,9 +339,23 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int
       double t = 0.0;
 #pragma unroll
       for (int i = 0; i < kScanThreads / 32; ++i) t += s_x2[threadIdx.x][i];
-      chi2[c * nmix + a0 + threadIdx.x] = t;
+      if (!kChunked)
+        chi2[c * nmix + a0 + threadIdx.x] = t;
+      else
+        w.partial[(c * nmix + a0 + threadIdx.x) * nbc + bc] = t;
     }
   }
+}
+
+// chi2[p] = sum of the point's bin-chunk partials in chunk order (k_scan_expand2, nbc > 1)
+__global__ void __launch_bounds__(128) k_scan_chi2_fold(const double* __restrict__ partial,
+                                                        int64_t npoints, int64_t nbc,
+                                                        double* __restrict__ chi2) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npoints) return;
+  double t = 0.0;
+  for (int64_t j = 0; j < nbc; ++j) t += partial[p * nbc + j];
+  chi2[p] = t;
 }
 
 }  // namespace
