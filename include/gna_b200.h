@@ -234,11 +234,12 @@ int gna_gl_integrate_ex(const gna_osc_params* p, double L_km, const double* d_ed
 
 /* ---------------------------------------------------------------------------
  * gna_fit_pattern_search — NEXT-4 (second part): a chi^2 minimiser that stays on the
- * GPU (the minimisation of P:446-451), driving the batch kernels.  Deterministic
- * compass search over x = (theta12, theta13, dm2_21, dm2_31): each iteration
- * evaluates chi^2 of the 81 points x_c + s * {-1, 0, +1}^4 (baselines, bins, order
- * and data as in gna_oscprob_batch), moves x_c to the argmin (lowest index on ties)
- * or halves s when x_c is already best.  Everything is stream-ordered (no host
+ * GPU (the minimisation of P:446-451).  Deterministic compass search over
+ * x = (theta12, theta13, dm2_21, dm2_31): each iteration evaluates chi^2 of the 81
+ * points x_c + s * {-1, 0, +1}^4 (baselines, bins, order and data as in
+ * gna_oscprob_batch) — a 9 x 9 product of (theta12, theta13) and (dm2_21, dm2_31)
+ * values, evaluated with the separable scan of gna_oscprob_scan — moves x_c to the
+ * argmin (lowest index on ties) or halves s when x_c is already best.  Everything is stream-ordered (no host
  * synchronisation), so the niter iterations can be captured in one CUDA graph.
  * d_state: device [8] = x_c[4] followed by s[4], updated in place.
  * d_hist: device [niter] best chi^2 after each iteration, or NULL.
