@@ -298,7 +298,11 @@ int gna_oscprob_scan(const gna_scan_grid* g, const double* L_km, const double* o
  * picks a default (eval: 4 Mi energies, GL: 1 Mi bins, batch: ~8 MiB of spectra
  * per chunk, or a single chunk when only chi^2 is requested; the batch uploads all
  * points and builds the node tables once per call).  Pinned (page-locked) host
- * arrays give full PCIe speed; pageable ones work but copy synchronously.
+ * arrays give full PCIe speed; pageable ones work but copy synchronously.  Batch
+ * spectra in page-locked memory (and chunk_points = 0) are stored by the kernel
+ * straight into host memory over PCIe during the one launch over all points — unless
+ * the points-across-lanes kernel runs (<= 2 baselines and >= 256 points), whose
+ * scattered stores are staged instead.
  * Returns after the results are in host memory (also on error).
  * ------------------------------------------------------------------------- */
 int gna_oscprob_eval_host(const gna_osc_params* p, double L_km, const double* h_E, int64_t n,

@@ -567,6 +567,9 @@ int launch_eval(const Coef& c, const double* E, int64_t n, double* P, cudaStream
 // c+2's H2D run at the same time (the paper's "CUDA Streams ... overlapped execution,
 // asynchronous memory copying") while every kernel still gets the whole GPU.
 constexpr int kRing = 3;
+#ifndef GNA_HOST_DIRECT
+#define GNA_HOST_DIRECT 1  // batch spectra stored by the kernel into page-locked host memory
+#endif
 #ifndef GNA_HOST_SPECTRA_MAX
 #define GNA_HOST_SPECTRA_MAX (1ull << 31)  // device bytes for un-ringed batch spectra staging
 #endif
@@ -1099,6 +1102,23 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   Staging* S = &g_stage[dev];
   if ((rc = stage_init(S))) return rc;
   const int64_t P = h_pts->npoints;
+  // Page-locked spectra (cudaHostAlloc / cudaHostRegister, mapped into the unified address
+  // space): the kernel stores the spectra straight into host memory over PCIe while it
+  // computes — one launch over all points, no staging copy to overlap (GNA_HOST_DIRECT)
+  // Only for the kernels whose spectra stores are whole rows of consecutive bins (per-point
+  // and points-inner); the points-across-lanes kernel (<= 2 baselines, >= GNA_BATCH_PT_MIN_POINTS
+  // points) stores one bin of 32 different rows per warp instruction, which over PCIe is
+  // ~30x slower than staging (cfg4: 5.4 vs 60 G energy points/s end to end).
+  const bool pt_kernel = GNA_BATCH_PT && nbase <= 2 && h_pts->npoints >= GNA_BATCH_PT_MIN_POINTS;
+  bool direct = false;
+  if (GNA_HOST_DIRECT && h_spectra && chunk_points <= 0 && !pt_kernel) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h_spectra) == cudaSuccess)
+      direct = at.type == cudaMemoryTypeHost && at.devicePointer == (void*)h_spectra;
+    else
+      cudaGetLastError();  // pageable memory: clear the error, use the staged pipeline
+  }
+  if (direct) chunk_points = P;
   if (chunk_points <= 0) {
     // ~8 MiB of spectra per chunk (their D2H overlaps the next chunks' kernels), at least 1
     // point; without spectra there is nothing large to overlap: one launch over all points
@@ -1119,7 +1139,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
   const size_t b_all = align16((size_t)P * nbins * 8);
   const bool out_ring = h_spectra && b_all > host_spectra_max();
   const size_t b_slot = h_spectra ? align16((size_t)chunk_points * nbins * 8) : 0;
-  const size_t b_spec = !h_spectra ? 0 : out_ring ? kRing * b_slot : b_all;
+  const size_t b_spec = (!h_spectra || direct) ? 0 : out_ring ? kRing * b_slot : b_all;
   if ((rc = ensure(&S->buf, &S->cap, tb + b_edges + b_data + b_pts + b_chi + b_ws + b_spec)))
     return rc;
   char* q = (char*)S->buf;
@@ -1156,6 +1176,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
         const gna_param_batch dp = {d_pts + o, d_pts + P + o, d_pts + 2 * P + o,
                                     d_pts + 3 * P + o, m};
         double* dspec = !h_spectra ? nullptr
+                        : direct   ? h_spectra + o * nbins  // mapped host memory
                         : out_ring ? (double*)(d_slots + r * b_slot)
                                    : (double*)d_slots + o * nbins;
         return launch_batch(&dp, L_km, omega, nbase, d_edges, nbins, order, dspec, d_data,
@@ -1164,7 +1185,7 @@ int gna_oscprob_batch_host(const gna_param_batch* h_pts, const double* L_km, con
       [&](int64_t ci, int r, cudaStream_t s) {
         const int64_t o = off[ci], m = rows(ci);
         int r2 = GNA_OK;
-        if (h_spectra)
+        if (h_spectra && !direct)
           r2 = d2h_copy(h_spectra + o * nbins,
                         out_ring ? (const void*)(d_slots + r * b_slot)
                                  : (const void*)((double*)d_slots + o * nbins),

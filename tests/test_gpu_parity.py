@@ -733,6 +733,23 @@ def test_gl_integrate_host_bitwise_equals_device(gna):
         assert np.array_equal(bh, bd)
 
 
+@pytest.mark.parametrize("P,nbase", [(300, 3), (7, 8), (300, 1)])
+def test_batch_host_pinned_spectra_bitwise_equals_device(gna, P, nbase):
+    """Page-locked spectra: the per-point / points-inner kernels store the spectra straight
+    into mapped host memory (GNA_HOST_DIRECT, one launch); the points-across-lanes case
+    (300 x 1) stays staged.  Both give the device call's bits."""
+    import torch
+    g = synth.rng(55 + P + nbase)
+    pts, L, om, edges, data = _batch_case(g, P, nbase, 257, 6)
+    spec = torch.empty((P, 257), dtype=torch.float64).pin_memory()
+    chi2 = torch.empty(P, dtype=torch.float64).pin_memory()
+    spec.numpy().fill(np.nan)
+    sph, x2h = gna.oscprob_batch_host(pts, L, om, edges, 6, data=data, spectra=spec.numpy(),
+                                      chi2=chi2.numpy())
+    spd, x2d = _run_batch(gna, pts, L, om, edges, 6, data)
+    assert np.array_equal(sph, spd) and np.array_equal(x2h, x2d)
+
+
 def test_batch_host_bitwise_equals_device(gna):
     g = synth.rng(52)
     pts, L, om, edges, data = _batch_case(g, 11, 3, 257, 6)
