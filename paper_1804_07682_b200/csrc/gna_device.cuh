@@ -7,7 +7,7 @@
 //   u  = f * f                  DMUL
 //   v  = V(u)                   7 DFMA (minimax of degree 7 in u, |err| <= 1.11e-15, V(0) = -1/2
 //                               exactly; sin2_poly.h.  GNA_SIN2_DEG 8: 8 DFMA, |err| <= 1.1e-16)
-//   acc += w * ((-1)^q v)       DFMA  (sign of v flipped with 2 integer ops on its hi word)
+//   acc += w * ((-1)^q v)       DFMA  (sign of v flipped by one IMAD on its hi word, flip_by_parity)
 // = 12 (13) FP64-pipe instructions, exploiting sin^2((pi/2)(q+f)) = 1/2 + (-1)^q v(f),
 // v(f) = -cos(pi f)/2, so that sum_ij w_ij sin^2 = sum w_ij / 2 + sum w_ij (-1)^q v.
 // The reduction is exact for |y| < 2^51, i.e. |Delta| < pi * 2^50 (t then lies in
@@ -61,16 +61,33 @@ __device__ __forceinline__ double sin2_poly(double u) {
   return fma(p, u, c_sin2[0]);
 }
 
+// (-1)^q p, the parity of q being bit 0 of t's low word: hi(p) + lo(t) * 2^31 (mod 2^32) adds
+// 2^31 to p's high word — toggles its sign bit and nothing else — exactly when q is odd.  One
+// IMAD instead of a shift and an XOR (GNA_SIGN_IMAD; the same bits either way).
+#ifndef GNA_SIGN_IMAD
+#define GNA_SIGN_IMAD 1
+#endif
+__device__ __forceinline__ double flip_by_parity(double p, double t) {
+#if GNA_SIGN_IMAD
+  unsigned hi;
+  asm("mad.lo.u32 %0, %1, 0x80000000, %2;"
+      : "=r"(hi)
+      : "r"((unsigned)__double2loint(t)), "r"((unsigned)__double2hiint(p)));
+  return __hiloint2double((int)hi, __double2loint(p));
+#else
+  const int odd = __double2loint(t) << 31;
+  return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
+#endif
+}
+
 // (-1)^q * V(f^2) for y = kq * invE = q + f  (y itself is never rounded separately)
 __device__ __forceinline__ double sin2c(double kq, double invE) {
   const double t = fma(kq, invE, kRoundMagic);
   const double q = t - kRoundMagic;
   const double f = fma(kq, invE, -q);
   const double u = f * f;
-  const double p = sin2_poly(u);
   // parity of q = bit 0 of t's low word -> sign bit of p
-  const int odd = __double2loint(t) << 31;
-  return __hiloint2double(__double2hiint(p) ^ odd, __double2loint(p));
+  return flip_by_parity(sin2_poly(u), t);
 }
 
 // Mixed tier.  The phase y = kq/E and its reduction stay
@@ -175,9 +192,7 @@ __device__ __forceinline__ double sin2_sin_c(double kq, double invE, double a, d
   r = fma(r, u, c_sinpi[1]);
   p = fma(p, u, c_sin2[0]);
   r = fma(r, u, c_sinpi[0]);
-  const double g = fma(b * f, r, a * p);
-  const int odd = __double2loint(t) << 31;
-  return __hiloint2double(__double2hiint(g) ^ odd, __double2loint(g));
+  return flip_by_parity(fma(b * f, r, a * p), t);
 }
 
 // Per-call coefficients of one (parameter point, baseline): P_ee (the hot path).

@@ -70,6 +70,7 @@ VARIANTS = {
     "gl_split_bw2_mb5": dict(GNA_GL_SPLIT_BW=2, GNA_GL_SPLIT_MINB=5),
     "fit_batch": dict(GNA_FIT_SCAN=0),
     "host_staged": dict(GNA_HOST_DIRECT=0),
+    "sign_lop": dict(GNA_SIGN_IMAD=0),
     "scan_a5": dict(GNA_SCAN_A=5),
     "scan_a2": dict(GNA_SCAN_A=2),
     "scan_a3": dict(GNA_SCAN_A=3),
