@@ -329,10 +329,21 @@ int launch_batch_k(const gna_param_batch* pts, const double* L_km, const double*
 #if GNA_BATCH_PT_MIXED_N10
     if (kMixed && order % 10 == 0)
       kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed> : k_oscprob_batch_pt<10, 6, kOut, kMixed>;
+#if GNA_BATCH_PT_ORD10
+    if (kMixed && order == 10)
+      kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed, 10>
+                       : k_oscprob_batch_pt<10, 6, kOut, kMixed, 10>;
+#endif
 #endif
 #if GNA_BATCH_PT_N10
     if (order % 10 == 0)
       kpt = nterm == 3 ? k_oscprob_batch_pt<10, 3, kOut, kMixed> : k_oscprob_batch_pt<10, 6, kOut, kMixed>;
+#endif
+#if GNA_BATCH_PT_ORD10
+    // GL10 (the reactor configurations): the order as a compile-time constant
+    if (!kMixed && order == 10)
+      kpt = nterm == 3 ? k_oscprob_batch_pt<5, 3, kOut, kMixed, 10>
+                       : k_oscprob_batch_pt<5, 6, kOut, kMixed, 10>;
 #endif
     const int64_t ng = (pts->npoints + 31) / 32;
     size_t smem_pt = (size_t)(2 * order + 3) * 32 * sizeof(double);

@@ -490,6 +490,19 @@ __global__ void __launch_bounds__(32, GNA_BATCH_PI_MINB) k_oscprob_batch_pi(
 #ifndef GNA_BATCH_PT_MIN_POINTS
 #define GNA_BATCH_PT_MIN_POINTS 256
 #endif
+// GNA_BATCH_PT_EH: a node's 1/E and h w staged as one double2 (one 16-byte shared load per node
+// instead of two 8-byte ones); GNA_BATCH_PT_ORD10: order 10 compiled as a constant (node loops
+// unrolled, shared-memory offsets immediate).  Same arithmetic, same bits.
+#ifndef GNA_BATCH_PT_EH
+#define GNA_BATCH_PT_EH 0
+#endif
+#ifndef GNA_BATCH_PT_ORD10
+#define GNA_BATCH_PT_ORD10 1
+#endif
+// node i of the tile's bin b in the staged node table: (1/E, h w) pairs or two planes
+__device__ __forceinline__ double pt_iE(const double* __restrict__ sE, int i, int b) {
+  return GNA_BATCH_PT_EH ? sE[2 * (i * 32 + b)] : sE[i * 32 + b];
+}
 
 // kShared (fp64 only): every point of the warp has the same (2,1) phase slope per baseline
 // (the same dm2_21 and L: a scan over theta13 / dm2_31 with the solar parameters fixed, as in
@@ -503,10 +516,17 @@ __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&
                                          const float (&wf)[NT], const double* __restrict__ sE,
                                          const double* __restrict__ sH, int b, int i, double& A,
                                          const double* __restrict__ sS = nullptr, int order = 0) {
-  double iE[N], a[N];
+  double iE[N], a[N], hw[N];
 #pragma unroll
   for (int n = 0; n < N; ++n) {
-    iE[n] = sE[(i + n) * 32 + b];
+    if constexpr (GNA_BATCH_PT_EH) {
+      const double2 eh = reinterpret_cast<const double2*>(sE)[(i + n) * 32 + b];
+      iE[n] = eh.x;
+      hw[n] = eh.y;
+    } else {
+      iE[n] = sE[(i + n) * 32 + b];
+      hw[n] = 0.0;
+    }
     a[n] = 0.0;
   }
   if constexpr (kMixed) {
@@ -554,7 +574,7 @@ __device__ __forceinline__ void pt_nodes(const double (&kq)[NT], const double (&
     }
   }
 #pragma unroll
-  for (int n = 0; n < N; ++n) A = fma(sH[(i + n) * 32 + b], a[n], A);
+  for (int n = 0; n < N; ++n) A = fma(GNA_BATCH_PT_EH ? hw[n] : sH[(i + n) * 32 + b], a[n], A);
 }
 
 template <int N, int NT, bool kMixed, bool kShared = false>
@@ -578,7 +598,7 @@ __device__ __forceinline__ void pt_tail(int r, const double (&kq)[NT], const dou
 // kMode 0: a full tile (no bounds checks); 1: bins at or past nbins are skipped; 2: every
 // bin is computed and those at or past nbins are dropped (x2 = 0 for them in both cases, as
 // in k_oscprob_batch).
-template <int kMode, int N, int NT, int kOut, bool kMixed, bool kShared = false>
+template <int kMode, int N, int NT, int kOut, bool kMixed, bool kShared = false, int kOrd = 0>
 __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (&cw)[NT],
                                           const float (&wf)[NT], double c0,
                                           const double* __restrict__ sE,
@@ -597,11 +617,18 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
     x2 = 0.0;
     if (kMode != 1 || k0 + b < nbins) {
       double A = 0.0;
-      int i = 0;
-      for (; i + N <= order; i += N)
-        pt_nodes<N, NT, kMixed, kShared>(kq, cw, wf, sE, sH, b, i, A, sS, order);
-      if (i < order)
-        pt_tail<N, NT, kMixed, kShared>(order - i, kq, cw, wf, sE, sH, b, i, A, sS, order);
+      if constexpr (kOrd > 0) {
+        static_assert(kOrd % N == 0, "kOrd");
+#pragma unroll
+        for (int i = 0; i < kOrd; i += N)
+          pt_nodes<N, NT, kMixed, kShared>(kq, cw, wf, sE, sH, b, i, A, sS, kOrd);
+      } else {
+        int i = 0;
+        for (; i + N <= order; i += N)
+          pt_nodes<N, NT, kMixed, kShared>(kq, cw, wf, sE, sH, b, i, A, sS, order);
+        if (i < order)
+          pt_tail<N, NT, kMixed, kShared>(order - i, kq, cw, wf, sE, sH, b, i, A, sS, order);
+      }
       const double s = fma(c0, sW[b], -A);
       if (kMode != 2 || k0 + b < nbins) {
         if (out && pact) out_store<kOut>(out + k0 + b, s);
@@ -625,15 +652,17 @@ __device__ __forceinline__ double pt_tile(const double (&kq)[NT], const double (
 // A tile may be split into S = 2^(5 - lv) sub-tiles of 2^lv consecutive visits (more,
 // shorter warps: a smaller last wave); each sub-tile's tree sum is a chi2 sub-partial and
 // k_chi2_reduce<S> finishes the tree's top levels.
-template <int N, int NT, int kOut, bool kMixed = false>
+template <int N, int NT, int kOut, bool kMixed = false, int kOrd = 0>
 __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BATCH_PT_MINB)
     k_oscprob_batch_pt(
     int order, int64_t nbins, int64_t npoints, int64_t bpp, int lv, BatchWs w,
     double* __restrict__ spectra, const double* __restrict__ data) {
   extern __shared__ double s_pt[];
-  double* sE = s_pt;                // [order][32] 1/E of the tile's nodes
-  double* sH = sE + order * 32;     // [order][32] h w
-  double* sW = sH + order * 32;     // [32] sum_i h w_i (same order as k_oscprob_batch)
+  if constexpr (kOrd > 0) order = kOrd;
+  // [order][32] 1/E and h w of the tile's nodes: interleaved pairs (GNA_BATCH_PT_EH) or planes
+  double* sE = s_pt;
+  double* sH = GNA_BATCH_PT_EH ? sE + 1 : sE + order * 32;
+  double* sW = s_pt + 2 * order * 32;  // [32] sum_i h w_i (same order as k_oscprob_batch)
   double* sD = sW + 32;             // [32] data
   double* sID = sD + 32;            // [32] 1 / data
   double* sS = sID + 32;            // [NT/3][order][32] shared sin^2 Delta_21 (fp64) or W (fp32)
@@ -658,8 +687,13 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
     double W = 0.0;
     for (int i = 0; i < order; ++i) {
       const double h = w.hw[(int64_t)i * nbins + kk];
-      sE[i * 32 + lane] = w.invE[(int64_t)i * nbins + kk];
-      sH[i * 32 + lane] = h;
+      const double iEk = w.invE[(int64_t)i * nbins + kk];
+      if constexpr (GNA_BATCH_PT_EH) {
+        reinterpret_cast<double2*>(sE)[i * 32 + lane] = make_double2(iEk, h);
+      } else {
+        sE[i * 32 + lane] = iEk;
+        sH[i * 32 + lane] = h;
+      }
       W += h;
     }
     sW[lane] = W;
@@ -692,9 +726,9 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
         for (int i = 0; i < order; ++i) {
           if constexpr (kMixed)
             sSf[((j / 3) * order + i) * 32 + lane] =
-                gna::cos2_w(gna::mixed_h1(kq[j], sE[i * 32 + lane]));
+                gna::cos2_w(gna::mixed_h1(kq[j], pt_iE(sE, i, lane)));
           else
-            sS[((j / 3) * order + i) * 32 + lane] = gna::sin2c(kq[j], sE[i * 32 + lane]);
+            sS[((j / 3) * order + i) * 32 + lane] = gna::sin2c(kq[j], pt_iE(sE, i, lane));
         }
       __syncwarp();
     }
@@ -707,23 +741,23 @@ __global__ void __launch_bounds__(32, kMixed ? GNA_BATCH_PT_MIXED_MINB : GNA_BAT
   double x2;
   if constexpr (kMixed) {
     if (shared)
-      x2 = pt_tile<2, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+      x2 = pt_tile<2, N, NT, kOut, kMixed, true, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
                                                  nbins, out, pact, sub, lv, sS);
     else
-      x2 = pt_tile<2, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+      x2 = pt_tile<2, N, NT, kOut, kMixed, false, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
                                            nbins, out, pact, sub, lv);
   }
   else if (shared)
     x2 = k0 + 32 <= nbins
-             ? pt_tile<0, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
+             ? pt_tile<0, N, NT, kOut, kMixed, true, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
                                                      k0, nbins, out, pact, sub, lv, sS)
-             : pt_tile<1, N, NT, kOut, kMixed, true>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
+             : pt_tile<1, N, NT, kOut, kMixed, true, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order,
                                                      k0, nbins, out, pact, sub, lv, sS);
   else
     x2 = k0 + 32 <= nbins
-             ? pt_tile<0, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+             ? pt_tile<0, N, NT, kOut, kMixed, false, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
                                                nbins, out, pact, sub, lv)
-             : pt_tile<1, N, NT, kOut, kMixed>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
+             : pt_tile<1, N, NT, kOut, kMixed, false, kOrd>(kq, cw, wf, c0, sE, sH, sW, sD, sID, order, k0,
                                                nbins, out, pact, sub, lv);
   if (w.partial && pact) w.partial[(p * warps_per_point_dev(nbins) + wt) * S + sub] = x2;
   if constexpr (kOut != kOutLocal) __threadfence_system();

@@ -71,6 +71,8 @@ VARIANTS = {
     "fit_batch": dict(GNA_FIT_SCAN=0),
     "host_staged": dict(GNA_HOST_DIRECT=0),
     "sign_lop": dict(GNA_SIGN_IMAD=0),
+    "pt_eh": dict(GNA_BATCH_PT_EH=1),
+    "pt_noord": dict(GNA_BATCH_PT_ORD10=0),
     "scan_a5": dict(GNA_SCAN_A=5),
     "scan_a2": dict(GNA_SCAN_A=2),
     "scan_a3": dict(GNA_SCAN_A=3),
