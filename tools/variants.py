@@ -72,6 +72,9 @@ VARIANTS = {
     "host_staged": dict(GNA_HOST_DIRECT=0),
     "sign_lop": dict(GNA_SIGN_IMAD=0),
     "pt_eh": dict(GNA_BATCH_PT_EH=1),
+    "b_ju1": dict(GNA_BATCH_JUNROLL=1),
+    "b_ju3": dict(GNA_BATCH_JUNROLL=3),
+    "b_ju4": dict(GNA_BATCH_JUNROLL=4),
     "pt_noord": dict(GNA_BATCH_PT_ORD10=0),
     "scan_a5": dict(GNA_SCAN_A=5),
     "scan_a2": dict(GNA_SCAN_A=2),
