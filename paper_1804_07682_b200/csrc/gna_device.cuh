@@ -259,15 +259,22 @@ __device__ __forceinline__ double2 prob_pair(const Coef& c, double iE0, double i
 }
 
 // H energies at once, term-major: every coefficient feeds H independent chains (ILP = H).
-// The term loop is deliberately not unrolled: one basic block per term keeps ptxas from
-// serialising the H chains to save registers (it does so in fully unrolled straight-line
-// code); the coefficient is picked with selects, not a dynamically indexed parameter.
+// Round 1 kept the term loop rolled (one basic block per term, the coefficient picked with
+// selects) because ptxas serialised the H chains of the unrolled form in the lane-pair kernel;
+// with the one-IMAD sign flip the unrolled form (GNA_PROB_TERM_UNROLL 3) is faster for the
+// thread-per-bin and warp-split GL kernels — the rolled loop spent ~14 instructions per term on
+// loop control and coefficient selects (10^5 bins x GL10 back to back 4.01 -> 3.94 us, 10^6
+// bins 27.8 -> 26.2 us; elementwise unchanged; profiles/variants_r02/term_unroll/).
+#ifndef GNA_PROB_TERM_UNROLL
+#define GNA_PROB_TERM_UNROLL 3
+#endif
+constexpr int kProbTermUnroll = GNA_PROB_TERM_UNROLL;
 template <int H>
 __device__ __forceinline__ void prob_inv_n(const PeeCoef& c, const double (&iE)[H], double (&P)[H]) {
   double acc[H];
 #pragma unroll
   for (int i = 0; i < H; ++i) acc[i] = 0.0;
-#pragma unroll 1
+#pragma unroll kProbTermUnroll
   for (int j = 0; j < 3; ++j) {
     const double kq = j == 0 ? c.kq[0] : (j == 1 ? c.kq[1] : c.kq[2]);
     const double w = j == 0 ? c.w[0] : (j == 1 ? c.w[1] : c.w[2]);

@@ -188,17 +188,22 @@ def _ipc_writer(rank, world, q_buf, q_done, P, nb):
 
     import paper_1804_07682_b200 as gna
     from paper_1804_07682_b200 import dist as gdist
-    torch.cuda.set_device(0)
-    sp_root, x2_root = q_buf.get()
-    pts, L, om, edges, order, data = _case(P=P, nbins=nb)
-    lo, hi = gdist.shard_range(P, world, rank)
-    f64 = dict(dtype=torch.float64, device="cuda")
-    mine = {k: torch.tensor(v[lo:hi], **f64) for k, v in pts.items()}
-    gna.oscprob_batch_ex(mine, L, om, torch.tensor(edges, **f64), order,
-                         sp_root.data_ptr() + lo * nb * 8, x2_root.data_ptr() + lo * 8,
-                         gna.GNA_OUT_PEER, data=torch.tensor(data, **f64))
-    torch.cuda.synchronize()
-    q_done.put(rank)
+    import traceback
+    try:
+        torch.cuda.set_device(0)
+        sp_root, x2_root = q_buf.get()
+        pts, L, om, edges, order, data = _case(P=P, nbins=nb)
+        lo, hi = gdist.shard_range(P, world, rank)
+        f64 = dict(dtype=torch.float64, device="cuda")
+        mine = {k: torch.tensor(v[lo:hi], **f64) for k, v in pts.items()}
+        gna.oscprob_batch_ex(mine, L, om, torch.tensor(edges, **f64), order,
+                             sp_root.data_ptr() + lo * nb * 8, x2_root.data_ptr() + lo * 8,
+                             gna.GNA_OUT_PEER, data=torch.tensor(data, **f64))
+        torch.cuda.synchronize()
+        q_done.put(rank)
+    except BaseException:  # reported to the root instead of a silent child exit
+        q_done.put("rank %d: %s" % (rank, traceback.format_exc()))
+        return
     q_buf.get()  # keep the mapping alive until the root has read the result
 
 
@@ -235,7 +240,21 @@ def test_peer_epilogue_writes_another_process_buffer_one_gpu(tmp_path):
                          order, sp.data_ptr() + lo * nb * 8, x2.data_ptr() + lo * 8,
                          gna.GNA_OUT_PEER, data=dd)
     torch.cuda.synchronize()
-    done = sorted(q_done.get(timeout=300) for _ in procs)
+    # collect the writers' hand-offs; a child that died (or reported an exception) fails the
+    # test at once instead of after the timeout
+    import queue
+    import time
+    done, t0 = [], time.monotonic()
+    while len(done) < len(procs):
+        try:
+            done.append(q_done.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, "writer exited with %s" % dead
+            assert time.monotonic() - t0 < 300, "writers did not finish in 300 s"
+    errs = [d for d in done if isinstance(d, str)]
+    assert not errs, "\n".join(errs)
+    done = sorted(done)
     assert done == list(range(1, world))
     got_sp, got_x2 = sp.cpu().numpy(), x2.cpu().numpy()
     for _ in procs:

@@ -73,6 +73,7 @@ VARIANTS = {
     "sign_lop": dict(GNA_SIGN_IMAD=0),
     "pt_eh": dict(GNA_BATCH_PT_EH=1),
     "b_ju1": dict(GNA_BATCH_JUNROLL=1),
+    "term_rolled": dict(GNA_PROB_TERM_UNROLL=1),
     "b_ju3": dict(GNA_BATCH_JUNROLL=3),
     "b_ju4": dict(GNA_BATCH_JUNROLL=4),
     "pt_noord": dict(GNA_BATCH_PT_ORD10=0),
