@@ -472,6 +472,7 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
                 : (order % 4 == 0) ? k_scan_setup<4>
                 : (order % 3 == 0) ? k_scan_setup<3>
                                    : k_scan_setup<GNA_SCAN_G_DEFAULT>;
+  if (GNA_SCAN_ORD10 && order == 10) ksetup = k_scan_setup<5, 10>;
   ksetup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
       a, g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges, chi2 ? data : nullptr, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -79,11 +79,14 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
 // G[ij] of one (mass point, bin): sum_b omega_b h sum_i w_i sin^2 Delta_ij, nodes in groups of
 // kG (the kG reciprocals and 3 kG sin^2 terms independent chains), each term folded over the
 // nodes in ascending order.
-template <int kG>
+// kOrd > 0: the order as a compile-time constant (GNA_SCAN_ORD10: GL10), node loop unrolled
+// and the GL nodes / weights constant-bank operands; the same operations in the same order.
+template <int kG, int kOrd = 0>
 __device__ __forceinline__ void scan_bin_G(const ScanArgs& a, double m21, double m31,
                                            double ctr, double h, double wsum, double& G0,
                                            double& G1, double& G2) {
-  const int off = GNA_GL_OFF(a.order);
+  const int order = kOrd > 0 ? kOrd : a.order;
+  const int off = GNA_GL_OFF(order);
   const double m32 = m31 - m21;
   G0 = 0.0, G1 = 0.0, G2 = 0.0;
   for (int b = 0; b < a.nbase; ++b) {
@@ -91,8 +94,9 @@ __device__ __forceinline__ void scan_bin_G(const ScanArgs& a, double m21, double
     const double k1 = phase_slope(m31, a.L[b]);
     const double k2 = phase_slope(m32, a.L[b]);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-    for (int i0 = 0; i0 < a.order; i0 += kG) {
-      const int n = a.order - i0 < kG ? a.order - i0 : kG;
+#pragma unroll
+    for (int i0 = 0; i0 < order; i0 += kG) {
+      const int n = order - i0 < kG ? order - i0 : kG;
       double v0[kG], v1[kG], v2[kG];
 #pragma unroll
       for (int i = 0; i < kG; ++i) {
@@ -122,6 +126,7 @@ __device__ __forceinline__ void scan_bin_G(const ScanArgs& a, double m21, double
 __device__ __forceinline__ double gl_wsum(int order) {
   const int off = GNA_GL_OFF(order);
   double wsum = 0.0;
+#pragma unroll
   for (int i = 0; i < order; ++i) wsum += c_gl_w[off + i];
   return wsum;
 }
@@ -134,8 +139,14 @@ __device__ __forceinline__ void scan_wmix(double th12, double th13, double* wm) 
   wm[3] = 0.0;
 }
 
-template <int kG>
-__global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
+#ifndef GNA_SCAN_ORD10
+#define GNA_SCAN_ORD10 1
+#endif
+#ifndef GNA_SCAN_SETUP_MINB
+#define GNA_SCAN_SETUP_MINB 1
+#endif
+template <int kG, int kOrd = 0>
+__global__ void __launch_bounds__(128, GNA_SCAN_SETUP_MINB) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
                                                     const double* __restrict__ th13,
                                                     const double* __restrict__ d21,
                                                     const double* __restrict__ d31,
@@ -149,9 +160,9 @@ __global__ void __launch_bounds__(128) k_scan_setup(ScanArgs a, const double* __
     const double e0 = edges[k], e1 = edges[k + 1];
     const double ctr = 0.5 * (e0 + e1);
     const double h = 0.5 * (e1 - e0);
-    const double wsum = gl_wsum(a.order);
+    const double wsum = gl_wsum(kOrd > 0 ? kOrd : a.order);
     double G0, G1, G2;
-    scan_bin_G<kG>(a, d21[c], d31[c], ctr, h, wsum, G0, G1, G2);
+    scan_bin_G<kG, kOrd>(a, d21[c], d31[c], ctr, h, wsum, G0, G1, G2);
     double* g = w.G + (c * 3) * a.nbins + k;
     g[0] = G0;
     g[a.nbins] = G1;

@@ -74,6 +74,9 @@ VARIANTS = {
     "pt_eh": dict(GNA_BATCH_PT_EH=1),
     "b_ju1": dict(GNA_BATCH_JUNROLL=1),
     "term_rolled": dict(GNA_PROB_TERM_UNROLL=1),
+    "scan_noord": dict(GNA_SCAN_ORD10=0),
+    "scan_ord_mb6": dict(GNA_SCAN_SETUP_MINB=6),
+
     "b_ju3": dict(GNA_BATCH_JUNROLL=3),
     "b_ju4": dict(GNA_BATCH_JUNROLL=4),
     "pt_noord": dict(GNA_BATCH_PT_ORD10=0),
