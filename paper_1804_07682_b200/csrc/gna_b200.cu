@@ -227,6 +227,29 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, si
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// scan and scan-fit kernels (k_scan_*, k_fit_grid, k_fit_update_grid): PDL when GNA_PDL_SCAN;
+// each of them executes pdl_launch_dependents + pdl_wait on entry, before any load or store,
+// so only the next kernel's launch and block rasterisation overlap this one's tail (stage B
+// after stage A, and the fit's five kernels per iteration)
+#ifndef GNA_PDL_SCAN
+#define GNA_PDL_SCAN 1
+#endif
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl_scan(void (*kern)(KArgs...), unsigned grid, unsigned block,
+                            cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (GNA_PDL && GNA_PDL_SCAN) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // single-point kernels (GL, elementwise): PDL when GNA_PDL_SINGLE (they wait before their
 // first input load, gna_common.cuh), else a plain stream-ordered launch
 template <class... KArgs, class... Args>
@@ -473,32 +496,36 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
                 : (order % 3 == 0) ? k_scan_setup<3>
                                    : k_scan_setup<GNA_SCAN_G_DEFAULT>;
   if (GNA_SCAN_ORD10 && order == 10) ksetup = k_scan_setup<5, 10>;
-  ksetup<<<(unsigned)((nsetup + 127) / 128), 128, 0, s>>>(
-      a, g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges, chi2 ? data : nullptr, w);
+  const int64_t nthr = nsetup;
+  cudaError_t e = launch_pdl_scan(ksetup, (unsigned)((nthr + 127) / 128), 128, s, a,
+                                  g->theta12, g->theta13, g->dm2_21, g->dm2_31, edges,
+                                  chi2 ? data : nullptr, w);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
   const bool vec2 = (nbins & 1) == 0 && ((uintptr_t)spectra & 15) == 0 &&
                     (!chi2 || ((uintptr_t)data & 15) == 0);
+  const double* dchi = chi2 ? data : nullptr;
   if (GNA_SCAN_EXPAND2 && vec2) {
     // bin chunks only when the grid gives fewer than 4 blocks per SM on its own
     const int64_t nbc = nblk < 4 * sm_count() ? scan_nbc(nbins) : 1;
     if (nblk * nbc > 0x7fffffffLL) return GNA_EINVAL;
     if (nbc > 1)
-      k_scan_expand2<true><<<(unsigned)(nblk * nbc), kScanThreads, 0, s>>>(
-          g->nmix, nbins, nchunk, w, spectra, chi2 ? data : nullptr, chi2);
+      e = launch_pdl_scan(k_scan_expand2<true>, (unsigned)(nblk * nbc), kScanThreads, s,
+                          g->nmix, nbins, nchunk, w, spectra, dchi, chi2);
     else
-      k_scan_expand2<false><<<(unsigned)nblk, kScanThreads, 0, s>>>(
-          g->nmix, nbins, nchunk, w, spectra, chi2 ? data : nullptr, chi2);
-    if (chi2 && nbc > 1) {
+      e = launch_pdl_scan(k_scan_expand2<false>, (unsigned)nblk, kScanThreads, s, g->nmix,
+                          nbins, nchunk, w, spectra, dchi, chi2);
+    if (e == cudaSuccess && chi2 && nbc > 1) {
       g_launches.fetch_add(1, std::memory_order_relaxed);
       const int64_t np = g->nmass * g->nmix;
-      k_scan_chi2_fold<<<(unsigned)((np + 127) / 128), 128, 0, s>>>(w.partial, np, nbc, chi2);
+      e = launch_pdl_scan(k_scan_chi2_fold, (unsigned)((np + 127) / 128), 128, s,
+                          (const double*)w.partial, np, nbc, chi2);
     }
   } else
-    k_scan_expand<<<(unsigned)nblk, kScanThreads, 0, s>>>(g->nmix, nbins, nchunk, w, spectra,
-                                                          chi2 ? data : nullptr, chi2);
+    e = launch_pdl_scan(k_scan_expand, (unsigned)nblk, kScanThreads, s, g->nmix, nbins, nchunk,
+                        w, spectra, dchi, chi2);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) return cuda_fail(e);
   e = cudaGetLastError();
   return e == cudaSuccess ? GNA_OK : cuda_fail(e);
 }
@@ -991,16 +1018,17 @@ int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbas
     const gna_scan_grid g = {grid, grid + kFitGrid, kFitGrid, grid + 2 * kFitGrid,
                              grid + 3 * kFitGrid, kFitGrid};
     if (niter > 0) {
-      k_fit_grid<<<1, 128, 0, s>>>(d_state, grid);
+      cudaError_t e = launch_pdl_scan(k_fit_grid, 1, 128, s, (const double*)d_state, grid);
       g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (e != cudaSuccess) return cuda_fail(e);
     }
     for (int it = 0; it < niter; ++it) {
       if ((rc = launch_scan(&g, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data, chi2,
                             sws, s)))
         return rc;
-      k_fit_update_grid<<<1, 128, 0, s>>>(d_state, grid, chi2, d_hist, it, it + 1 < niter);
+      cudaError_t e = launch_pdl_scan(k_fit_update_grid, 1, 128, s, d_state, grid,
+                                      (const double*)chi2, d_hist, it, (int)(it + 1 < niter));
       g_launches.fetch_add(1, std::memory_order_relaxed);
-      cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return cuda_fail(e);
     }
     return GNA_OK;

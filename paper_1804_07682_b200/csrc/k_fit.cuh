@@ -102,6 +102,8 @@ __device__ __forceinline__ void fit_grid(const double* __restrict__ state,
 
 __global__ void __launch_bounds__(128) k_fit_grid(const double* __restrict__ state,
                                                   double* __restrict__ grid) {
+  pdl_launch_dependents();
+  pdl_wait();  // launched with PDL (GNA_PDL_SCAN): the predecessor's writes are visible
   fit_grid(state, grid, threadIdx.x);
 }
 
@@ -115,6 +117,8 @@ __global__ void __launch_bounds__(128) k_fit_update_grid(double* __restrict__ st
   __shared__ double s_v[128];
   __shared__ int s_i[128];
   const int t = threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();  // launched with PDL (GNA_PDL_SCAN): stage B's chi^2 is complete and visible
   s_v[t] = t < kFitCand ? chi2[t] : INFINITY;
   s_i[t] = t;
   __syncthreads();

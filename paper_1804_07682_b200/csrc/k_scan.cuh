@@ -81,40 +81,49 @@ ScanWs scan_ws_carve(void* base, int64_t nmix, int64_t nmass, int64_t nbins) {
 // nodes in ascending order.
 // kOrd > 0: the order as a compile-time constant (GNA_SCAN_ORD10: GL10), node loop unrolled
 // and the GL nodes / weights constant-bank operands; the same operations in the same order.
+// s_ij(b) = sum_i w_i (-1)^q v of one baseline b (the three pairs share each node's reciprocal)
+template <int kG, int kOrd = 0>
+__device__ __forceinline__ void scan_base_s(const ScanArgs& a, int b, double m21, double m31,
+                                            double m32, double ctr, double h, double& s0,
+                                            double& s1, double& s2) {
+  const int order = kOrd > 0 ? kOrd : a.order;
+  const int off = GNA_GL_OFF(order);
+  const double k0 = phase_slope(m21, a.L[b]);
+  const double k1 = phase_slope(m31, a.L[b]);
+  const double k2 = phase_slope(m32, a.L[b]);
+  s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int i0 = 0; i0 < order; i0 += kG) {
+    const int n = order - i0 < kG ? order - i0 : kG;
+    double v0[kG], v1[kG], v2[kG];
+#pragma unroll
+    for (int i = 0; i < kG; ++i) {
+      const double invE = gna::rcp(fma(h, c_gl_t[off + i0 + (i < n ? i : 0)], ctr));
+      v0[i] = gna::sin2c(k0, invE);
+      v1[i] = gna::sin2c(k1, invE);
+      v2[i] = gna::sin2c(k2, invE);
+    }
+#pragma unroll
+    for (int i = 0; i < kG; ++i) {
+      if (i < n) {
+        const double wi = c_gl_w[off + i0 + i];
+        s0 = fma(wi, v0[i], s0);
+        s1 = fma(wi, v1[i], s1);
+        s2 = fma(wi, v2[i], s2);
+      }
+    }
+  }
+}
+
 template <int kG, int kOrd = 0>
 __device__ __forceinline__ void scan_bin_G(const ScanArgs& a, double m21, double m31,
                                            double ctr, double h, double wsum, double& G0,
                                            double& G1, double& G2) {
-  const int order = kOrd > 0 ? kOrd : a.order;
-  const int off = GNA_GL_OFF(order);
   const double m32 = m31 - m21;
   G0 = 0.0, G1 = 0.0, G2 = 0.0;
   for (int b = 0; b < a.nbase; ++b) {
-    const double k0 = phase_slope(m21, a.L[b]);
-    const double k1 = phase_slope(m31, a.L[b]);
-    const double k2 = phase_slope(m32, a.L[b]);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-    for (int i0 = 0; i0 < order; i0 += kG) {
-      const int n = order - i0 < kG ? order - i0 : kG;
-      double v0[kG], v1[kG], v2[kG];
-#pragma unroll
-      for (int i = 0; i < kG; ++i) {
-        const double invE = gna::rcp(fma(h, c_gl_t[off + i0 + (i < n ? i : 0)], ctr));
-        v0[i] = gna::sin2c(k0, invE);
-        v1[i] = gna::sin2c(k1, invE);
-        v2[i] = gna::sin2c(k2, invE);
-      }
-#pragma unroll
-      for (int i = 0; i < kG; ++i) {
-        if (i < n) {
-          const double wi = c_gl_w[off + i0 + i];
-          s0 = fma(wi, v0[i], s0);
-          s1 = fma(wi, v1[i], s1);
-          s2 = fma(wi, v2[i], s2);
-        }
-      }
-    }
+    double s0, s1, s2;
+    scan_base_s<kG, kOrd>(a, b, m21, m31, m32, ctr, h, s0, s1, s2);
     // h sum_i w_i sin^2 = h (W/2 + sum_i w_i (-1)^q v)
     const double ob = a.omega[b] * h;
     G0 = fma(ob, fma(0.5, wsum, s0), G0);
@@ -143,7 +152,7 @@ __device__ __forceinline__ void scan_wmix(double th12, double th13, double* wm) 
 #define GNA_SCAN_ORD10 1
 #endif
 #ifndef GNA_SCAN_SETUP_MINB
-#define GNA_SCAN_SETUP_MINB 1
+#define GNA_SCAN_SETUP_MINB 3
 #endif
 template <int kG, int kOrd = 0>
 __global__ void __launch_bounds__(128, GNA_SCAN_SETUP_MINB) k_scan_setup(ScanArgs a, const double* __restrict__ th12,
@@ -152,6 +161,10 @@ __global__ void __launch_bounds__(128, GNA_SCAN_SETUP_MINB) k_scan_setup(ScanArg
                                                     const double* __restrict__ d31,
                                                     const double* __restrict__ edges,
                                                     const double* __restrict__ data, ScanWs w) {
+  // PDL (GNA_PDL_SCAN): stage B may be scheduled now; nothing is read or written before the
+  // predecessor (the fit's grid update, or the previous call) has completed
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = a.nmass * a.nbins;
   if (t < n1) {
@@ -199,6 +212,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand(int64_t nmix, int6
                                                               const double* __restrict__ data,
                                                               double* __restrict__ chi2) {
   __shared__ double s_x2[kScanA][kScanThreads / 32];
+  pdl_launch_dependents();
+  pdl_wait();  // stage A's G, H, 1/D and mixing weights are complete and visible
   const int64_t c = blockIdx.x / nchunk;
   const int64_t a0 = (blockIdx.x - c * nchunk) * kScanA;
   const int na = (int)min((int64_t)kScanA, nmix - a0);
@@ -283,6 +298,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int
                                                                const double* __restrict__ data,
                                                                double* __restrict__ chi2) {
   __shared__ double s_x2[kScanA][kScanThreads / 32];
+  pdl_launch_dependents();
+  pdl_wait();  // stage A's G, H, 1/D and mixing weights are complete and visible
   const int64_t nbc = kChunked ? scan_nbc(nbins) : 1;
   const int64_t cb = kChunked ? blockIdx.x / nbc : blockIdx.x;  // (mass point, mixing chunk)
   const int64_t bc = kChunked ? blockIdx.x - cb * nbc : 0;      // bin chunk
@@ -362,6 +379,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int
 __global__ void __launch_bounds__(128) k_scan_chi2_fold(const double* __restrict__ partial,
                                                         int64_t npoints, int64_t nbc,
                                                         double* __restrict__ chi2) {
+  pdl_launch_dependents();
+  pdl_wait();  // every chunk partial of stage B is written
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npoints) return;
   double t = 0.0;

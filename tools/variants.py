@@ -85,6 +85,10 @@ VARIANTS = {
     "scan_a3": dict(GNA_SCAN_A=3),
     "scan_t64": dict(GNA_SCAN_THREADS=64),
     "scan_noexp2": dict(GNA_SCAN_EXPAND2=0),
+    "nopdl_scan": dict(GNA_PDL_SCAN=0),
+    "scan_mb1": dict(GNA_SCAN_SETUP_MINB=1),
+    "scan_mb2": dict(GNA_SCAN_SETUP_MINB=2),
+    "scan_mb4": dict(GNA_SCAN_SETUP_MINB=4),
     "ev_stg": dict(GNA_EVAL_BULK_STORE=0),
     "ev_bulk": dict(GNA_EVAL_BULK_STORE=1),
     "ev_bulk_s6m5": dict(GNA_EVAL_BULK_STORE=1, GNA_EVAL_STAGES=5, GNA_EVAL_MINB=5),
@@ -95,7 +99,7 @@ KERNELS = [r"k_oscprob_eval_tmaIN3gna7PeeCoef", r"k_oscprob_batchILi1ELi5ELi0ELb
            r"k_oscprob_batch_piILi5ELi0ELi0ELb0E", r"k_oscprob_batch_piILi5ELi0ELi3ELb0E",
            r"k_oscprob_batchILi1ELi5ELi0ELb1E", r"k_oscprob_batch_piILi5ELi0ELi3ELb1E",
            r"k_oscprob_batchILi1ELi10ELi0ELb1E", r"k_gl_integrate_splitILi10EN3gna7PeeCoef",
-           r"k_gl_integrate_tbILi10EN3gna7PeeCoef", r"k_scan_expand", r"k_oscprob_batch_ptILi5ELi3ELi0ELb0E"]
+           r"k_gl_integrate_tbILi10EN3gna7PeeCoef", r"k_scan_expand", r"k_scan_setupILi5ELi10E", r"k_oscprob_batch_ptILi5ELi3ELi0ELb0E"]
 
 
 def main(names):
