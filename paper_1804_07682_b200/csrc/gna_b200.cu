@@ -507,7 +507,7 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
   const double* dchi = chi2 ? data : nullptr;
   if (GNA_SCAN_EXPAND2 && vec2) {
     // bin chunks only when the grid gives fewer than 4 blocks per SM on its own
-    const int64_t nbc = nblk < 4 * sm_count() ? scan_nbc(nbins) : 1;
+    const int64_t nbc = nblk < GNA_SCAN_CHUNK_BPSM * sm_count() ? scan_nbc(nbins) : 1;
     if (nblk * nbc > 0x7fffffffLL) return GNA_EINVAL;
     if (nbc > 1)
       e = launch_pdl_scan(k_scan_expand2<true>, (unsigned)(nblk * nbc), kScanThreads, s,

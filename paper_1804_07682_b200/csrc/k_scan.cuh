@@ -37,7 +37,13 @@ struct ScanWs {
 // stage B splits the bins into chunks of kScanBinChunk (even) when the grid alone gives too few
 // blocks (the fit's 9 x 9 stencil: 27 blocks for 10^4 bins); chi^2 is then summed from
 // per-chunk partials in chunk order (k_scan_chi2_fold)
-constexpr int64_t kScanBinChunk = 1024;
+#ifndef GNA_SCAN_BIN_CHUNK
+#define GNA_SCAN_BIN_CHUNK 512
+#endif
+#ifndef GNA_SCAN_CHUNK_BPSM
+#define GNA_SCAN_CHUNK_BPSM 4  // chunk the bins when the grid has fewer blocks per SM than this
+#endif
+constexpr int64_t kScanBinChunk = GNA_SCAN_BIN_CHUNK;
 __host__ __device__ inline int64_t scan_nbc(int64_t nbins) {
   return (nbins + kScanBinChunk - 1) / kScanBinChunk;
 }

@@ -680,7 +680,9 @@ def _scan_case(g, nmix, nmass, nbase, nbins, order):
 @pytest.mark.parametrize("nmix,nmass,nbase,nbins,order", [
     (1, 1, 1, 1, 1), (7, 5, 3, 37, 4), (3, 4, 8, 300, 10), (2, 2, 64, 50, 32), (33, 1, 1, 257, 5),
     # GL10 (stage A compiled for the order) with 2..7 baselines and ragged grids
-    (5, 3, 2, 51, 10), (4, 3, 3, 77, 10), (2, 7, 5, 129, 10), (6, 1, 7, 13, 10)])
+    (5, 3, 2, 51, 10), (4, 3, 3, 77, 10), (2, 7, 5, 129, 10), (6, 1, 7, 13, 10),
+    # a small grid over more bins than one stage-B chunk: chi^2 from chunk partials (ragged)
+    (3, 2, 2, 1100, 10)])
 def test_scan_vs_oracle_on_expanded_grid(gna, nmix, nmass, nbase, nbins, order):
     g = synth.rng(500 + nmix * nmass + nbins)
     grid, L, om, edges, data = _scan_case(g, nmix, nmass, nbase, nbins, order)
