@@ -200,8 +200,11 @@ __global__ void __launch_bounds__(128, GNA_SCAN_SETUP_MINB) k_scan_setup(ScanArg
 // G[c][*][k], H[k], D[k], 1/D[k] of its bins once and writes T for all kScanA points
 // (coalesced rows), so G is read once per chunk instead of once per point; chi2 of each
 // point is reduced in the block (fixed shuffle tree + warps in order) and written directly.
+// spectra stored with the evict-first hint (st.global.cs): the 80 MB written once stream through
+// L2 without displacing G, H, D, 1/D (cfg4grid 26.96 -> 26.72 us mean over 3 x 200 steps,
+// profiles/variants_r02/scan3/summary.txt); the same values
 #ifndef GNA_SCAN_STREAMING_STORES
-#define GNA_SCAN_STREAMING_STORES 0
+#define GNA_SCAN_STREAMING_STORES 1
 #endif
 #ifndef GNA_SCAN_A
 #define GNA_SCAN_A 4
@@ -351,7 +354,11 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_expand2(int64_t nmix, int
         double2 T;
         T.x = H.x - fma(w0[j], G0.x, fma(w1[j], G1.x, w2[j] * G2.x));
         T.y = H.y - fma(w0[j], G0.y, fma(w1[j], G1.y, w2[j] * G2.y));
+#if GNA_SCAN_STREAMING_STORES
+        if (out) __stcs(out + j * np + q, T);
+#else
         if (out) out[j * np + q] = T;
+#endif
         const double dx = T.x - D.x, dy = T.y - D.y;
         x2[j] = fma(dx * dx, iD.x, x2[j]);
         x2[j] = fma(dy * dy, iD.y, x2[j]);
