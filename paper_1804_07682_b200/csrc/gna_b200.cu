@@ -468,9 +468,14 @@ int launch_batch(const gna_param_batch* pts, const double* L_km, const double* o
 #undef GNA_LB
 }
 
+// fold_out (the fit, GNA_FIT_FOLD): when stage B leaves chi^2 as bin-chunk partials, skip
+// k_scan_chi2_fold and report the partials (and their count per point) so the caller's next
+// kernel folds them itself, in the same order
 int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega, int32_t nbase,
                 const double* edges, int64_t nbins, int32_t order, double* spectra,
-                const double* data, double* chi2, void* workspace, cudaStream_t s) {
+                const double* data, double* chi2, void* workspace, cudaStream_t s,
+                const double** fold_out = nullptr, int64_t* fold_nbc = nullptr) {
+  if (fold_out) *fold_out = nullptr;
   ScanArgs a;
   std::memset(&a, 0, sizeof(a));
   double om = 0.0;
@@ -515,7 +520,10 @@ int launch_scan(const gna_scan_grid* g, const double* L_km, const double* omega,
     else
       e = launch_pdl_scan(k_scan_expand2<false>, (unsigned)nblk, kScanThreads, s, g->nmix,
                           nbins, nchunk, w, spectra, dchi, chi2);
-    if (e == cudaSuccess && chi2 && nbc > 1) {
+    if (e == cudaSuccess && chi2 && nbc > 1 && fold_out) {
+      *fold_out = w.partial;
+      *fold_nbc = nbc;
+    } else if (e == cudaSuccess && chi2 && nbc > 1) {
       g_launches.fetch_add(1, std::memory_order_relaxed);
       const int64_t np = g->nmass * g->nmix;
       e = launch_pdl_scan(k_scan_chi2_fold, (unsigned)((np + 127) / 128), 128, s,
@@ -1023,11 +1031,14 @@ int gna_fit_pattern_search(const double* L_km, const double* omega, int32_t nbas
       if (e != cudaSuccess) return cuda_fail(e);
     }
     for (int it = 0; it < niter; ++it) {
+      const double* part = nullptr;
+      int64_t nbc = 0;
       if ((rc = launch_scan(&g, L_km, omega, nbase, d_edges, nbins, order, nullptr, d_data, chi2,
-                            sws, s)))
+                            sws, s, GNA_FIT_FOLD ? &part : nullptr, &nbc)))
         return rc;
       cudaError_t e = launch_pdl_scan(k_fit_update_grid, 1, 128, s, d_state, grid,
-                                      (const double*)chi2, d_hist, it, (int)(it + 1 < niter));
+                                      (const double*)chi2, part, nbc, d_hist, it,
+                                      (int)(it + 1 < niter));
       g_launches.fetch_add(1, std::memory_order_relaxed);
       if (e != cudaSuccess) return cuda_fail(e);
     }

@@ -109,17 +109,35 @@ __global__ void __launch_bounds__(128) k_fit_grid(const double* __restrict__ sta
 
 // argmin + move/halve as k_fit_update; the best candidate's coordinates are rebuilt from the
 // old state (the same fma as fit_candidate), then the next grid is written
+// GNA_FIT_FOLD: with partial != nullptr the chi^2 of candidate t is folded here from stage B's
+// nbc bin-chunk partials in chunk order — k_scan_chi2_fold's sum, one launch per iteration fewer
+#ifndef GNA_FIT_FOLD
+#define GNA_FIT_FOLD 1
+#endif
 __global__ void __launch_bounds__(128) k_fit_update_grid(double* __restrict__ state,
                                                          double* __restrict__ grid,
                                                          const double* __restrict__ chi2,
+                                                         const double* __restrict__ partial,
+                                                         int64_t nbc,
                                                          double* __restrict__ hist, int iter,
                                                          int next_grid) {
   __shared__ double s_v[128];
+  __shared__ double s_c[kFitCand];
   __shared__ int s_i[128];
   const int t = threadIdx.x;
   pdl_launch_dependents();
   pdl_wait();  // launched with PDL (GNA_PDL_SCAN): stage B's chi^2 is complete and visible
-  s_v[t] = t < kFitCand ? chi2[t] : INFINITY;
+  double x = INFINITY;
+  if (t < kFitCand) {
+    if (partial) {
+      x = 0.0;
+      for (int64_t j = 0; j < nbc; ++j) x += partial[t * nbc + j];
+    } else {
+      x = chi2[t];
+    }
+    s_c[t] = x;
+  }
+  s_v[t] = x;
   s_i[t] = t;
   __syncthreads();
   for (int o = 64; o > 0; o >>= 1) {  // argmin, ties -> lowest index (deterministic)
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(128) k_fit_update_grid(double* __restrict__ st
   if (t == 0) {
     const int best = s_i[0];
     const int centre = kFitCand / 2;
-    if (best == centre || !(s_v[0] < chi2[centre])) {
+    if (best == centre || !(s_v[0] < s_c[centre])) {
 #pragma unroll
       for (int d = 0; d < kFitDim; ++d) state[kFitDim + d] *= 0.5;
     } else {
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(128) k_fit_update_grid(double* __restrict__ st
 #pragma unroll
       for (int d = 0; d < kFitDim; ++d) state[d] = nc[d];
     }
-    if (hist) hist[iter] = fmin(s_v[0], chi2[centre]);
+    if (hist) hist[iter] = fmin(s_v[0], s_c[centre]);
   }
   if (next_grid) {
     __syncthreads();  // thread 0's state update is complete

@@ -87,6 +87,7 @@ VARIANTS = {
     "scan_noexp2": dict(GNA_SCAN_EXPAND2=0),
     "nopdl_scan": dict(GNA_PDL_SCAN=0),
     "scan_mb1": dict(GNA_SCAN_SETUP_MINB=1),
+    "fit_nofold": dict(GNA_FIT_FOLD=0),
     "scan_stcs": dict(GNA_SCAN_STREAMING_STORES=1),
     "scan_ch256": dict(GNA_SCAN_BIN_CHUNK=256, GNA_SCAN_CHUNK_BPSM=64),
     "scan_ch512": dict(GNA_SCAN_BIN_CHUNK=512, GNA_SCAN_CHUNK_BPSM=64),
