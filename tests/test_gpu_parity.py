@@ -976,11 +976,11 @@ def test_fused_gather_epilogue_single_rank(gna, P, nbase):
 
 
 # ------------------------------------------------------------------------ on-GPU fit loop
-def _fit_case(sign=1.0):
+def _fit_case(sign=1.0, nbins=500):
     # sign = -1: inverted-ordering truth (signed dm2_31)
     truth = np.array([0.5838, 0.1496, 7.53e-5, sign * 2.52e-3])
     L, om = np.array([52.5, 53.0]), np.array([1.0, 0.98])
-    edges = synth.uniform_edges(500, 1.0, 10.0)
+    edges = synth.uniform_edges(nbins, 1.0, 10.0)
     pts = dict(theta12=truth[:1], theta13=truth[1:2], dm2_21=truth[2:3], dm2_31=truth[3:4])
     data, _ = oracle.batch(pts, L, om, edges, 5, nthreads=_nt())  # pseudo-data = oracle at truth
     return truth, L, om, edges, data[0]
@@ -1000,14 +1000,16 @@ def test_fit_pattern_search_recovers_truth(gna, sign):
     assert np.all(np.abs(x - truth) <= 1e-6 * np.abs(truth)), (x, truth)
 
 
-@pytest.mark.parametrize("sign", [1.0, -1.0])
-def test_fit_pattern_search_steps_match_host_compass_search_on_oracle_chi2(gna, sign):
+# nbins 500: stage B in one bin chunk; 1500: three chunks (chi^2 from partials); 501: odd, the
+# scalar stage B + the update kernel — the argmin/update runs in stage B's last block otherwise
+@pytest.mark.parametrize("sign,nbins", [(1.0, 500), (-1.0, 500), (1.0, 1500), (1.0, 501)])
+def test_fit_pattern_search_steps_match_host_compass_search_on_oracle_chi2(gna, sign, nbins):
     """Each GPU iteration (niter = 1 calls) equals one compass step computed on the host:
     the 81 candidates centre + step * {-1, 0, 1}^4 (first coordinate fastest), their chi^2 from
     the oracle, argmin with ties to the lowest index; move there if it beats the centre, else
     halve the steps.  The state after every step must match bit for bit (normal and inverted
     ordering)."""
-    truth, L, om, edges, data = _fit_case(sign)
+    truth, L, om, edges, data = _fit_case(sign, nbins)
     step = np.array([0.01, 0.005, 2e-6, 5e-5])
     st = np.r_[truth + np.array([0.7, -0.6, 0.8, -0.5]) * step, step]
     de, dd = _t(edges), _t(data)
